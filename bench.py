@@ -1,0 +1,388 @@
+"""Bench: single-stream time steps/s of blocked SRU/QRNN inference vs T_b.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2] [--block 32] [--mode f32]
+
+One "step" = one pass of the hot path (a whole-sequence blocked forward,
+``rnnb_forward``) over the workload's synthetic input; the metric is time
+steps of the sequence per second, summed over GPUs.  Default workload is
+BASELINE.json configs[1] (cfg2: QRNN w=2, D=H=1024, L=2048, fp32), which the
+metric is quoted on; the headline T_b is --block and every T_b of the
+config's sweep is reported under "sweep".
+
+Timing: W untimed warm-up steps, then K steps each bracketed by CUDA events
+on the launching stream; L2 (126 MB) is flushed by writing a 256 MB buffer
+before every timed step (outside the events), so weights and inputs start
+cold in HBM each step.  Barrier + synchronize around the timed region, max
+over ranks.  nvidia-smi clocks are sampled during the timed region.  cfg2
+does not shard (single layer, single stream): N>1 runs N independent
+replicas (weak scaling).
+
+--impl reference times the reference algorithm on the host CPU cores (the
+C port of rnnblock's fast path under oracle/, all host threads) on a
+bounded prefix of the same workload; rank 0 only.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_1803_11389_b200 import workloads  # noqa: E402
+
+METRIC = "single-stream time steps/sec vs block size T_b"
+UNIT = "steps/s"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured (MEASURED_PEAKS.json)"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in self.rows:
+            for n, v in zip(names, r[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
+    """Dominant kernel = the fused layer kernel (one launch per layer)."""
+    L = w.seq_len
+    flops = workloads.flops_per_step(w) * L / launches_per_step
+    s_w = {"f32": 4, "tf32": 4, "bf16": 2, "f64": 8}[mode]
+    s_a = 8 if mode == "f64" else 4
+    params = workloads.param_count(w)
+    nblocks = -(-L // T_b)
+    # cold-cache traffic model (rnnblock traffic.py:26-27,64-68) + input/output once
+    bytes_model = (params * s_w * nblocks + (w.X.shape[1] + w.layers[-1].d_h) * s_a * L) / launches_per_step
+    sec = ms_per_launch / 1e3
+    mhz = pk.get("sm_max_mhz", 1965.0)
+    if mode in ("f32", "f64"):
+        # FFMA pipe: 148 SMs x 128 FP32 FMA/clk x 2 FLOP (fp64: half rate on B200)
+        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12 * (0.5 if mode == "f64" else 1.0)
+        pipe = "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)"
+        src = f"derived: 148 SMs x 128 lanes x 2 FLOP x sm_max_mhz {mhz:.0f} (no CUDA-core peak in MEASURED_PEAKS.json)"
+    else:
+        peak = pk["bf16_tflops"] * (0.5 if mode == "tf32" else 1.0)
+        pipe = "tcgen05 " + mode
+        src = "MEASURED_PEAKS.json bf16_tflops" + (" x 0.5 (tf32)" if mode == "tf32" else "")
+    achieved = flops / sec / 1e12
+    hbm = pk["hbm_gbs"]
+    return {
+        "bound": "tensor" if mode in ("bf16", "tf32") else "compute",
+        "pipe": pipe,
+        "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+        "frac": round(achieved / peak, 4), "peak_source": src,
+        "traffic": traffic,
+        "flops_per_launch": flops, "ms_per_launch": round(ms_per_launch, 5),
+        "hbm_model": {
+            "note": "reference cold-cache byte model (weights re-fetched every block); "
+                    "the kernel keeps the weight slice SMEM/L2-resident, so this exceeds real DRAM traffic",
+            "bytes_per_launch": bytes_model, "achieved_gbs": round(bytes_model / sec / 1e9, 1),
+            "peak_gbs": hbm, "frac": round(bytes_model / sec / 1e9 / hbm, 4)},
+    }
+
+
+def load_traffic(workload, T_b, mode):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(f"{workload}/{mode}/T{T_b}")
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1803_11389_b200 as P
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workloads.make(args.workload)
+    if w.bidirectional or w.proj is not None:
+        raise SystemExit(f"bench workload {args.workload} is not a plain stack yet")
+    st = P.DeviceStack(w.kind, w.layers, mode=args.mode, device=local_rank)
+    dt = st.dtype
+    X = torch.from_numpy(w.X.astype(st.np_dtype)).to(dev)
+    L = w.seq_len
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream()
+    blocks = list(w.block_sizes) if args.sweep else []
+    if args.block not in blocks:
+        blocks.append(args.block)
+    blocks = sorted(set(blocks))
+    out = torch.empty((L, st.d_h[-1]), dtype=dt, device=dev)
+
+    def one(T_b):
+        st.forward(X, T_b, out=out)
+
+    dist = world > 1
+    results = {}
+    sampler = None
+    for T_b in blocks:
+        headline = T_b == args.block
+        for _ in range(args.warmup):
+            one(T_b)
+        torch.cuda.synchronize()
+        launches = st.last_launches
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if dist:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        if headline and rank == 0:
+            sampler = ClockSampler(local_rank)
+            sampler.start()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush, outside the events
+            ev[i][0].record(stream)
+            one(T_b)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            torch.distributed.barrier()
+        clocks = sampler.stop() if (headline and sampler is not None) else None
+        ms = [a.elapsed_time(b) for a, b in ev]
+        ms_step = sum(ms) / len(ms)
+        if dist:
+            t = torch.tensor([ms_step], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms_step = float(t.item())
+        results[T_b] = {"ms_per_step": ms_step, "ms_min": min(ms), "launches": launches, "clocks": clocks}
+
+    # end-to-end through the public C-ABI host entry point (pinned host buffers)
+    Xh = torch.from_numpy(w.X.astype(st.np_dtype)).pin_memory()
+    Hh = torch.empty((L, st.d_h[-1]), dtype=dt).pin_memory()
+    Xn, Hn = Xh.numpy(), Hh.numpy()
+    for _ in range(max(1, args.warmup)):
+        st.forward_host(Xn, args.block, out=Hn)
+    if dist:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e_steps = max(3, min(args.steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        st.forward_host(Xn, args.block, out=Hn)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+    if dist:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    itemsize = np.dtype(st.np_dtype).itemsize
+    e2e = {"value": round(L * world / (e2e_ms / 1e3), 1), "unit": UNIT,
+           "h2d_bytes_per_step": int(L * w.X.shape[1] * itemsize),
+           "d2h_bytes_per_step": int(L * st.d_h[-1] * itemsize),
+           "ms_per_step": round(e2e_ms, 4), "api": "rnnb_forward_host (C ABI, pinned host X/H)"}
+
+    if rank != 0:
+        st.close()
+        return None
+    pk, pk_src = peaks()
+    sweep = {}
+    for T_b, r in results.items():
+        rf = roofline_for(w, T_b, args.mode, r["ms_per_step"] / (r["launches"] or 1), r["launches"] or 1,
+                          pk, load_traffic(args.workload, T_b, args.mode))
+        sweep[str(T_b)] = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
+                           "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"],
+                           "tflops": rf["achieved"], "hbm_model_frac": rf["hbm_model"]["frac"]}
+    head = results[args.block]
+    roof = roofline_for(w, args.block, args.mode, head["ms_per_step"] / (head["launches"] or 1),
+                        head["launches"] or 1, pk, load_traffic(args.workload, args.block, args.mode))
+    roof["peaks_file"] = pk_src
+    resident = [bool(st.query(3, li)) for li in range(st.n_layers)]
+    line = {
+        "metric": METRIC, "value": round(L * world / (head["ms_per_step"] / 1e3), 1), "unit": UNIT,
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(head["ms_per_step"], 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": {"f32": "f32", "f64": "f64", "bf16": "bf16", "tf32": "tf32"}[args.mode],
+        "data": "synthetic (seeded PCG64, BASELINE.json distributions)",
+        "config": {"workload": args.workload, "cell": w.kind.value, "d_in": int(w.X.shape[1]),
+                   "d_h": int(w.layers[-1].d_h), "n_layers": len(w.layers), "seq_len": L,
+                   "block_size": args.block, "mode": args.mode,
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed before every timed step (256 MB write)",
+                   "weights_smem_resident": resident,
+                   "units_per_cta": [st.query(2, li) for li in range(st.n_layers)],
+                   "grid": [st.query(4, li) for li in range(st.n_layers)]},
+        "e2e": e2e,
+        "gpu_launches": int(head["launches"] * args.steps),
+        "roofline": roof,
+        "sweep": sweep,
+        "clocks": head["clocks"],
+    }
+    if args.cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, w, sample_steps=args.cpu_sample)
+    st.close()
+    return line
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline: the oracle port of rnnblock's fast path
+
+
+def _oracle():
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle as O
+    O.lib()
+    return O
+
+
+def cpu_baseline(args, w, sample_steps):
+    O = _oracle()
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    L = min(sample_steps, w.seq_len)
+    X = np.ascontiguousarray(w.X[:L])
+    layers = [lay.mats() for lay in w.layers]
+    O.run_blocked(w.kind.value, layers, X, args.block)  # warm-up
+    times = []
+    t_end = time.perf_counter() + args.cpu_seconds
+    while time.perf_counter() < t_end or len(times) < 3:
+        t0 = time.perf_counter()
+        O.run_blocked(w.kind.value, layers, X, args.block)
+        times.append(time.perf_counter() - t0)
+    med = statistics.median(times)
+    return {"value": round(L / med, 1), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{args.workload} first {L} of {w.seq_len} steps, T_b={args.block}, "
+                      f"median of {len(times)} runs, oracle/ C port of rnnblock fast kernel, "
+                      f"OpenMP {cores} threads"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    w = workloads.make(args.workload)
+    O = _oracle()
+    cores = os.cpu_count() or 1
+    O.set_threads(cores)
+    L = min(args.cpu_sample, w.seq_len)
+    X = np.ascontiguousarray(w.X[:L])
+    layers = [lay.mats() for lay in w.layers]
+    for _ in range(args.warmup):
+        O.run_blocked(w.kind.value, layers, X, args.block)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.run_blocked(w.kind.value, layers, X, args.block)
+        ts.append(time.perf_counter() - t0)
+    ms = sum(ts) / len(ts) * 1e3
+    v = round(L / (ms / 1e3), 1)
+    sample = (f"{args.workload} first {L} of {w.seq_len} steps per step, T_b={args.block}; "
+              f"oracle/ C port of rnnblock's fast path (numba prange -> OpenMP), {cores} threads")
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded PCG64, BASELINE.json distributions)",
+            "config": {"workload": args.workload, "block_size": args.block, "mode": "f32",
+                       "seq_len_sample": L},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--block", type=int, default=32)
+    ap.add_argument("--mode", default="f32", choices=("f32", "f64", "bf16", "tf32"))
+    ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--cpu-sample", type=int, default=512, help="time steps in the CPU sample")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warning: W < 3 warm-up steps violates the timing rules; using 3")
+        args.warmup = 3
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        line = run_reference(args, rank, world)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_ours(args, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None and rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,124 @@
+/*
+ * rnnb.h -- C ABI of the B200-native blocked SRU/QRNN inference path.
+ *
+ * Drop-in boundary for rnnblock's blocked executor (arXiv 1803.11389 path,
+ * /root/reference/pkg/src/rnnblock).  Plain pointers and sizes only; no
+ * torch or C++ types cross this boundary and no C++ exception escapes it.
+ * Every call returns an rnnb_status; rnnb_last_error() gives a
+ * thread-local message for the last failing call on that thread.
+ *
+ * Reference interface each entry point replaces (file:line in rnnblock):
+ *
+ *   rnnb_stack_create / rnnb_stack_set_layer
+ *       RnnConfig (model_io.py:75-99) + WeightSet (model_io.py:102-110) with
+ *       SruWeights / QrnnWeights layers (cells.py:78-126).  The reference
+ *       re-stacks gate matrices on every call (blocked.py:196-197,238-245);
+ *       here they are repacked once into a device-resident, gate-interleaved
+ *       layout.
+ *   rnnb_forward / rnnb_forward_host
+ *       run_blocked(cfg, weights, X, block_size, ...)  blocked.py:221-268.
+ *       Layer-major like the reference; c and the QRNN x_carry are carried
+ *       across blocks (blocked.py:247-264) and, optionally, in/out across
+ *       calls (streaming use; the reference always starts from zero).
+ *   rnnb_gates
+ *       precompute_gates_sru / precompute_gates_qrnn  blocked.py:123-150
+ *       (and the stacked forms _sru_gates_stacked / _qrnn_gates_stacked,
+ *       blocked.py:200-218, which compute the same values).
+ *   rnnb_sweep      recurrence_sweep   blocked.py:165-176
+ *   rnnb_finalize   finalize_outputs   blocked.py:179-193
+ *   rnnb_plan_blocks  plan_blocks      blocked.py:38-50
+ *
+ * Errors mirror the reference's ValueError conditions (blocked.py:231-235,
+ * cells.py:86-93, kernels.py:34-47): RNNB_EINVAL.  CUDA failures:
+ * RNNB_ECUDA.
+ */
+#ifndef RNNB_H
+#define RNNB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RNNB_OK = 0,
+  RNNB_EINVAL = 1,       /* bad argument: the reference raises ValueError */
+  RNNB_ECUDA = 2,        /* CUDA runtime / launch failure */
+  RNNB_ENOMEM = 3,
+  RNNB_EUNSUPPORTED = 4  /* valid request this build does not handle */
+} rnnb_status;
+
+typedef enum { RNNB_SRU = 1, RNNB_QRNN = 2 } rnnb_cell;
+
+/* Compute modes.  F32/F64 match the reference's precisions (kernels.py:25)
+ * with accumulators of the element type.  BF16 stores weights as bf16 and
+ * rounds x to bf16 at the product (fp32 accumulate, fp32 gates/state/h);
+ * TF32 rounds weights and x to tf32 at the product (fp32 accumulate). */
+typedef enum { RNNB_F32 = 0, RNNB_F64 = 1, RNNB_BF16 = 2, RNNB_TF32 = 3 } rnnb_mode;
+
+typedef enum { RNNB_DT_F32 = 0, RNNB_DT_F64 = 1 } rnnb_dtype;
+
+typedef struct rnnb_stack* rnnb_stack_t;
+
+const char* rnnb_last_error(void);
+const char* rnnb_version(void);
+
+/* Number of blocks plan_blocks(L, T_b) yields: ceil(L / T_b) (blocked.py:38-50). */
+rnnb_status rnnb_plan_blocks(int64_t seq_len, int64_t block_size, int64_t* n_blocks,
+                             int64_t* last_len);
+
+/* A stack of n_layers cells of one kind on CUDA device `device`.
+ * d_in[l], d_h[l] per layer; layer l+1 must read width d_h[l]; SRU requires
+ * d_in == d_h (cells.py:89). */
+rnnb_status rnnb_stack_create(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
+                              const int64_t* d_h, int mode, int device);
+rnnb_status rnnb_stack_destroy(rnnb_stack_t h);
+
+/* Upload one layer.  mats[] are HOST row-major arrays in the reference's
+ * canonical field order (model_io.py:29-33):
+ *   SRU : w_cand, w_forget, w_highway [d_h x d_in], b_forget, b_highway [d_h]
+ *   QRNN: w_cand, w_cand_prev, w_forget, w_forget_prev, w_out, w_out_prev
+ * src_dtype: element type of mats (RNNB_DT_F32 / RNNB_DT_F64). */
+rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* mats, int n_mats,
+                                 int src_dtype);
+
+/* Whole-network blocked forward on DEVICE buffers (run_blocked).
+ *   X       [L x d_in(0)] rows = time steps, row stride ldx elements
+ *   H       [L x d_h(last)] output, row stride ldh
+ *   c_state optional [sum_l d_h(l)] in/out (NULL: zero in, not written)
+ *   x_carry optional [sum_l d_in(l)] in/out, QRNN x_{-1} per layer
+ * Element type: double for RNNB_F64 stacks, float otherwise.  stream is a
+ * cudaStream_t (NULL = legacy default stream). */
+rnnb_status rnnb_forward(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size,
+                         void* H, int64_t ldh, void* c_state, void* x_carry, void* stream);
+
+/* Same on HOST buffers: H2D of X, forward, D2H of H inside the call
+ * (pinned or pageable).  Synchronises the stream before returning. */
+rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t block_size,
+                              void* H, void* c_state, void* x_carry, void* stream);
+
+/* Unit-level ops on DEVICE buffers, one layer of the stack.
+ * rnnb_gates: Xt [l x d_in] (time-major block, row stride ldx), x_carry
+ * [d_in] or NULL (QRNN); G [3][d_h][ldg]: cand, forget, out_gate (gate
+ * values exactly as GateBlock, blocked.py:53-71). */
+rnnb_status rnnb_gates(rnnb_stack_t h, int layer, const void* Xt, int64_t ldx, int64_t l,
+                       const void* x_carry, void* G, int64_t ldg, void* stream);
+/* C[i,t] = f[i,t] c + (1-f[i,t]) cand[i,t], c = c_init[i] at t=0; all [d x T]. */
+rnnb_status rnnb_sweep(const void* forget, const void* cand, const void* c_init, void* C,
+                       int64_t d, int64_t T, int dtype, void* stream);
+/* QRNN: H = o tanh(C); SRU: H = o tanh(C) + (1-o) Xb; all [d x T]. */
+rnnb_status rnnb_finalize(int kind, const void* out_gate, const void* C, const void* Xb, void* H,
+                          int64_t d, int64_t T, int dtype, void* stream);
+
+/* Introspection for benches/tests. what: 0 = device weight bytes,
+ * 1 = kernel launches issued by the last forward, 2 = units per CTA of
+ * `layer`, 3 = 1 if the last forward kept `layer`'s weights resident in
+ * shared memory, 4 = grid size of `layer`, 5 = dynamic smem bytes. */
+rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RNNB_H */

@@ -1,0 +1,48 @@
+"""B200-native single-stream blocked SRU/QRNN inference (arXiv 1803.11389).
+
+Drop-in for the reference package's blocked path (rnnblock ``run_blocked``
+and its unit-level ops, types and trace contract).  All compute runs in
+hand-written sm_100a CUDA kernels in ``librnnb.so`` behind a C ABI
+(include/rnnb.h); there is no CPU fallback.
+
+Fast path: ``DeviceStack`` (weights resident in HBM, forward on device
+tensors).  Drop-in path: ``run_blocked(cfg, weights, X, block_size)``.
+"""
+
+from .blocked import (
+    PHASE_BIAS,
+    PHASE_GEMM,
+    PHASE_GEMV,
+    BlockPlan,
+    GateBlock,
+    KernelTrace,
+    TraceEvent,
+    finalize_outputs,
+    lstm_run_precomputed,
+    plan_blocks,
+    precompute_gates_qrnn,
+    precompute_gates_sru,
+    recurrence_sweep,
+    run_blocked,
+)
+from .cells import (
+    PRECISIONS,
+    CellKind,
+    CellState,
+    QrnnWeights,
+    RnnConfig,
+    SruWeights,
+    WeightSet,
+    zero_state,
+)
+from .device import DeviceStack
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "PHASE_BIAS", "PHASE_GEMM", "PHASE_GEMV", "BlockPlan", "GateBlock", "KernelTrace",
+    "TraceEvent", "finalize_outputs", "lstm_run_precomputed", "plan_blocks",
+    "precompute_gates_qrnn", "precompute_gates_sru", "recurrence_sweep", "run_blocked",
+    "PRECISIONS", "CellKind", "CellState", "QrnnWeights", "RnnConfig", "SruWeights",
+    "WeightSet", "zero_state", "DeviceStack",
+]

@@ -1,0 +1,73 @@
+"""ctypes binding of the in-tree CUDA library (include/rnnb.h).
+
+There is no CPU fallback: if ``librnnb.so`` is missing or CUDA is not
+available, every product entry point raises.  Build it with
+``python -m paper_1803_11389_b200.build`` (``__graft_entry__.build()``).
+"""
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librnnb.so")
+
+OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4
+SRU, QRNN = 1, 2
+MODES = {"f32": 0, "f64": 1, "bf16": 2, "tf32": 3}
+DT_F32, DT_F64 = 0, 1
+
+# every symbol include/rnnb.h declares (checked by tests/test_abi.py)
+SYMBOLS = (
+    "rnnb_last_error", "rnnb_version", "rnnb_plan_blocks", "rnnb_stack_create",
+    "rnnb_stack_destroy", "rnnb_stack_set_layer", "rnnb_forward", "rnnb_forward_host",
+    "rnnb_gates", "rnnb_sweep", "rnnb_finalize", "rnnb_query",
+)
+
+_lib = None
+
+
+class RnnbError(RuntimeError):
+    pass
+
+
+def load():
+    """Load librnnb.so (once).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RnnbError(f"{LIB_PATH} is not built; run `python -m paper_1803_11389_b200.build` "
+                        "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    P64 = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "rnnb_last_error": ([], ctypes.c_char_p),
+        "rnnb_version": ([], ctypes.c_char_p),
+        "rnnb_plan_blocks": ([i64, i64, P64, P64], ci),
+        "rnnb_stack_create": ([ctypes.POINTER(vp), ci, ci, P64, P64, ci, ci], ci),
+        "rnnb_stack_destroy": ([vp], ci),
+        "rnnb_stack_set_layer": ([vp, ci, ctypes.POINTER(vp), ci, ci], ci),
+        "rnnb_forward": ([vp, vp, i64, i64, i64, vp, i64, vp, vp, vp], ci),
+        "rnnb_forward_host": ([vp, vp, i64, i64, vp, vp, vp, vp], ci),
+        "rnnb_gates": ([vp, ci, vp, i64, i64, vp, vp, i64, vp], ci),
+        "rnnb_sweep": ([vp, vp, vp, vp, i64, i64, ci, vp], ci),
+        "rnnb_finalize": ([ci, vp, vp, vp, vp, i64, i64, ci, vp], ci),
+        "rnnb_query": ([vp, ci, ci, P64], ci),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def check(status):
+    """Map a status code to the reference's exception types."""
+    if status == OK:
+        return
+    msg = load().rnnb_last_error().decode(errors="replace")
+    if status == EINVAL:
+        raise ValueError(msg)
+    raise RnnbError(f"rnnb status {status}: {msg}")

@@ -1,0 +1,506 @@
+// C ABI of the blocked SRU/QRNN path (see include/rnnb.h).
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/rnnb.h"
+#include "ffma_dispatch.cuh"
+
+using namespace rnnb;
+
+namespace {
+
+thread_local std::string g_err;
+
+rnnb_status fail(rnnb_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+rnnb_status cuda_fail(cudaError_t e, const char* where) {
+  return fail(RNNB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+#define CUDA_TRY(expr)                                  \
+  do {                                                  \
+    cudaError_t _e = (expr);                            \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+struct Layer {
+  int64_t din = 0, dh = 0;
+  int Dp = 0;        // d_in padded to a multiple of 8
+  int U = 7;         // units per CTA
+  int Upad = 0;      // d_h padded to a multiple of U
+  void* W = nullptr; // [Upad*3][taps*Dp] gate-interleaved
+  void* bias = nullptr;
+  size_t wbytes = 0;
+  bool loaded = false;
+  FfmaPlan last;
+  int grid = 0;
+};
+
+}  // namespace
+
+struct rnnb_stack {
+  int kind = 0, n_layers = 0, mode = 0, device = 0, num_sms = 148;
+  std::vector<Layer> layers;
+  void* ws[2] = {nullptr, nullptr};
+  size_t ws_bytes = 0;
+  int64_t last_launches = 0;
+  void* hostX = nullptr;  // e2e device staging
+  void* hostH = nullptr;
+  size_t hx_bytes = 0, hh_bytes = 0;
+};
+
+namespace {
+
+size_t elem_size(int mode) { return mode == RNNB_F64 ? 8 : 4; }
+size_t wsize(int mode) { return mode == RNNB_F64 ? 8 : (mode == RNNB_BF16 ? 2 : 4); }
+int taps(int kind) { return kind == RNNB_QRNN ? 2 : 1; }
+
+int choose_units(int64_t dh, int num_sms) {
+  // enough CTAs to cover the SMs, U from the instantiated set {2, 4, 7}
+  if (dh >= 7LL * num_sms * 0.85) return 7;
+  if (dh >= 4LL * num_sms * 0.85) return 4;
+  if (dh > 2LL * num_sms) return 4;
+  return 2;
+}
+
+float to_tf32(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) {  // round-to-nearest, ties away (cvt.rna)
+    u += 0x1000u;
+    u &= 0xffffe000u;
+  }
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+uint16_t to_bf16(float v) {
+  uint32_t u;
+  std::memcpy(&u, &v, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return (uint16_t)((u >> 16) | ((u & 0xffff) ? 0x40 : 0));
+  u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
+  return (uint16_t)(u >> 16);
+}
+
+rnnb_status ensure_ws(rnnb_stack* h, size_t bytes) {
+  if (h->ws_bytes >= bytes) return RNNB_OK;
+  for (auto& p : h->ws)
+    if (p) cudaFree(p), p = nullptr;
+  h->ws_bytes = 0;
+  CUDA_TRY(cudaMalloc(&h->ws[0], bytes));
+  CUDA_TRY(cudaMalloc(&h->ws[1], bytes));
+  h->ws_bytes = bytes;
+  return RNNB_OK;
+}
+
+template <typename TA, typename TW>
+LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
+  LayerArgs<TA, TW> a{};
+  a.W = static_cast<const TW*>(ly.W);
+  a.bias = static_cast<const TA*>(ly.bias);
+  a.D = (int)ly.din;
+  a.Dp = ly.Dp;
+  a.H = (int)ly.dh;
+  a.xround = h->mode == RNNB_BF16 ? XR_BF16 : (h->mode == RNNB_TF32 ? XR_TF32 : XR_NONE);
+  return a;
+}
+
+// one layer over [L x din] -> [L x dh]
+template <typename TA, typename TW>
+rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_t L, int64_t Tb,
+                         TA* Hout, int64_t ldh, TA* c_io, TA* xc_io, TA* G, int64_t ldg,
+                         cudaStream_t s) {
+  Layer& ly = h->layers[li];
+  LayerArgs<TA, TW> a = make_args<TA, TW>(h, ly);
+  a.X = X;
+  a.ldx = ldx;
+  a.xcarry = h->kind == RNNB_QRNN ? xc_io : nullptr;
+  a.Xhw = X;
+  a.ldhw = ldx;
+  a.Hout = Hout;
+  a.ldh = ldh;
+  a.c_in = c_io;
+  a.c_out = c_io;
+  a.G = G;
+  a.ldg = ldg;
+  a.L = L;
+  a.T_b = (int)(Tb > (int64_t)1 << 30 ? (int64_t)1 << 30 : Tb);
+  FfmaPlan plan;
+  cudaError_t e = ffma_layer_run<TA, TW>(h->kind, ly.U, a, true, s, &plan);
+  if (e != cudaSuccess) return cuda_fail(e, "ffma_layer launch");
+  ly.last = plan;
+  ly.grid = (int)((ly.dh + ly.U - 1) / ly.U);
+  h->last_launches += 1;
+  return RNNB_OK;
+}
+
+template <typename TA, typename TW>
+rnnb_status forward_t(rnnb_stack* h, const TA* X, int64_t ldx, int64_t L, int64_t Tb, TA* H,
+                      int64_t ldh, TA* c_state, TA* x_carry, cudaStream_t s) {
+  int64_t maxw = 0;
+  for (auto& ly : h->layers) maxw = ly.dh > maxw ? ly.dh : maxw;
+  if (h->n_layers > 1) {
+    rnnb_status st = ensure_ws(h, (size_t)L * maxw * sizeof(TA));
+    if (st != RNNB_OK) return st;
+  }
+  h->last_launches = 0;
+  const TA* in = X;
+  int64_t ldin = ldx;
+  int64_t coff = 0, xoff = 0;
+  for (int li = 0; li < h->n_layers; ++li) {
+    Layer& ly = h->layers[li];
+    const bool last = li == h->n_layers - 1;
+    TA* out = last ? H : static_cast<TA*>(h->ws[li & 1]);
+    const int64_t ldo = last ? ldh : ly.dh;
+    TA* c_io = c_state ? c_state + coff : nullptr;
+    TA* xc_io = x_carry ? x_carry + xoff : nullptr;
+    rnnb_status st = layer_launch<TA, TW>(h, li, in, ldin, L, Tb, out, ldo, c_io, xc_io, nullptr, 0, s);
+    if (st != RNNB_OK) return st;
+    if (xc_io && h->kind == RNNB_QRNN) {
+      // carried x for the next call = last input row of this layer (blocked.py:262)
+      CUDA_TRY(cudaMemcpyAsync(xc_io, in + (L - 1) * ldin, ly.din * sizeof(TA), cudaMemcpyDeviceToDevice, s));
+      h->last_launches += 1;
+    }
+    coff += ly.dh;
+    xoff += ly.din;
+    in = out;
+    ldin = ldo;
+  }
+  return RNNB_OK;
+}
+
+rnnb_status check_stack(rnnb_stack* h) {
+  if (!h) return fail(RNNB_EINVAL, "null stack handle");
+  for (int i = 0; i < h->n_layers; ++i)
+    if (!h->layers[i].loaded) return fail(RNNB_EINVAL, "layer " + std::to_string(i) + " has no weights");
+  return RNNB_OK;
+}
+
+template <typename T>
+__global__ void sweep_kernel(const T* __restrict__ F, const T* __restrict__ Xh, const T* __restrict__ c0,
+                             T* __restrict__ C, int64_t d, int64_t T_) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= d) return;
+  T c = c0[i];
+  for (int64_t t = 0; t < T_; ++t) {
+    T f = F[i * T_ + t];
+    c = f * c + (T(1) - f) * Xh[i * T_ + t];
+    C[i * T_ + t] = c;
+  }
+}
+
+template <typename T>
+__global__ void finalize_kernel(int kind, const T* __restrict__ O, const T* __restrict__ C,
+                                const T* __restrict__ Xb, T* __restrict__ H, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T o = O[i];
+  T h = o * tanh_full(C[i]);
+  if (kind == RNNB_SRU) h = h + (T(1) - o) * Xb[i];
+  H[i] = h;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rnnb_last_error(void) { return g_err.c_str(); }
+const char* rnnb_version(void) { return "rnnb-b200 0.1.0 (sm_100a)"; }
+
+rnnb_status rnnb_plan_blocks(int64_t seq_len, int64_t block_size, int64_t* n_blocks, int64_t* last_len) {
+  if (seq_len < 1) return fail(RNNB_EINVAL, "seq_len must be >= 1");
+  if (block_size < 1) return fail(RNNB_EINVAL, "block_size must be >= 1");
+  int64_t nb = (seq_len + block_size - 1) / block_size;
+  if (n_blocks) *n_blocks = nb;
+  if (last_len) *last_len = seq_len - (nb - 1) * block_size;
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_stack_create(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
+                              const int64_t* d_h, int mode, int device) {
+  if (!out) return fail(RNNB_EINVAL, "out is null");
+  *out = nullptr;
+  if (kind != RNNB_SRU && kind != RNNB_QRNN)
+    return fail(RNNB_EINVAL, "blocked execution covers SRU and QRNN; use lstm_run_precomputed for LSTM");
+  if (n_layers < 1) return fail(RNNB_EINVAL, "n_layers must be >= 1");
+  if (mode < RNNB_F32 || mode > RNNB_TF32) return fail(RNNB_EINVAL, "unknown compute mode");
+  if (!d_in || !d_h) return fail(RNNB_EINVAL, "null dimension arrays");
+  for (int l = 0; l < n_layers; ++l) {
+    if (d_in[l] < 1 || d_h[l] < 1) return fail(RNNB_EINVAL, "d_in and d_h must be >= 1");
+    if (kind == RNNB_SRU && d_in[l] != d_h[l]) return fail(RNNB_EINVAL, "SRU requires d_in == d_h");
+    if (l > 0 && d_in[l] != d_h[l - 1])
+      return fail(RNNB_EINVAL, "layer " + std::to_string(l) + " input width does not match previous layer width");
+    if (d_in[l] > (1 << 24) || d_h[l] > (1 << 24)) return fail(RNNB_EUNSUPPORTED, "dimension too large");
+  }
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(RNNB_EINVAL, "bad device ordinal");
+  auto* h = new rnnb_stack();
+  h->kind = kind;
+  h->n_layers = n_layers;
+  h->mode = mode;
+  h->device = device;
+  cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+  h->layers.resize(n_layers);
+  for (int l = 0; l < n_layers; ++l) {
+    Layer& ly = h->layers[l];
+    ly.din = d_in[l];
+    ly.dh = d_h[l];
+    ly.Dp = (int)((d_in[l] + 7) / 8 * 8);
+    ly.U = choose_units(d_h[l], h->num_sms);
+    ly.Upad = (int)((d_h[l] + ly.U - 1) / ly.U * ly.U);
+  }
+  *out = h;
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
+  if (!h) return RNNB_OK;
+  int cur = 0;
+  cudaGetDevice(&cur);
+  cudaSetDevice(h->device);
+  for (auto& ly : h->layers) {
+    if (ly.W) cudaFree(ly.W);
+    if (ly.bias) cudaFree(ly.bias);
+  }
+  for (auto& p : h->ws)
+    if (p) cudaFree(p);
+  if (h->hostX) cudaFree(h->hostX);
+  if (h->hostH) cudaFree(h->hostH);
+  cudaSetDevice(cur);
+  delete h;
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* mats, int n_mats, int src_dtype) {
+  if (!h) return fail(RNNB_EINVAL, "null stack handle");
+  if (layer < 0 || layer >= h->n_layers) return fail(RNNB_EINVAL, "layer index out of range");
+  const int need = h->kind == RNNB_SRU ? 5 : 6;
+  if (!mats || n_mats != need) return fail(RNNB_EINVAL, "expected " + std::to_string(need) + " weight arrays");
+  if (src_dtype != RNNB_DT_F32 && src_dtype != RNNB_DT_F64) return fail(RNNB_EINVAL, "src dtype must be f32 or f64");
+  for (int i = 0; i < n_mats; ++i)
+    if (!mats[i]) return fail(RNNB_EINVAL, "null weight array");
+  Layer& ly = h->layers[layer];
+  const int T = taps(h->kind);
+  const int64_t Kp = (int64_t)T * ly.Dp;
+  const int64_t rows = (int64_t)ly.Upad * 3;
+  auto get = [&](int m, int64_t idx) -> double {
+    return src_dtype == RNNB_DT_F64 ? static_cast<const double*>(mats[m])[idx]
+                                    : (double)static_cast<const float*>(mats[m])[idx];
+  };
+  // canonical index of (gate g, tap) -> mats slot
+  auto slot = [&](int g, int tap) { return h->kind == RNNB_SRU ? g : 2 * g + tap; };
+  const size_t ws = wsize(h->mode);
+  std::vector<unsigned char> host((size_t)rows * Kp * ws, 0);
+  for (int64_t u = 0; u < ly.dh; ++u)
+    for (int g = 0; g < 3; ++g)
+      for (int tap = 0; tap < T; ++tap) {
+        const int m = slot(g, tap);
+        const int64_t r = 3 * u + g;
+        for (int64_t k = 0; k < ly.din; ++k) {
+          const double v = get(m, u * ly.din + k);
+          const size_t dst = (size_t)r * Kp + (size_t)tap * ly.Dp + k;
+          switch (h->mode) {
+            case RNNB_F64: reinterpret_cast<double*>(host.data())[dst] = v; break;
+            case RNNB_BF16: reinterpret_cast<uint16_t*>(host.data())[dst] = to_bf16((float)v); break;
+            case RNNB_TF32: reinterpret_cast<float*>(host.data())[dst] = to_tf32((float)v); break;
+            default: reinterpret_cast<float*>(host.data())[dst] = (float)v; break;
+          }
+        }
+      }
+  int cur = 0;
+  cudaGetDevice(&cur);
+  CUDA_TRY(cudaSetDevice(h->device));
+  if (ly.W) cudaFree(ly.W), ly.W = nullptr;
+  if (ly.bias) cudaFree(ly.bias), ly.bias = nullptr;
+  ly.wbytes = host.size();
+  CUDA_TRY(cudaMalloc(&ly.W, host.size()));
+  CUDA_TRY(cudaMemcpy(ly.W, host.data(), host.size(), cudaMemcpyHostToDevice));
+  if (h->kind == RNNB_SRU) {
+    const size_t es = elem_size(h->mode);
+    std::vector<unsigned char> b((size_t)ly.Upad * 2 * es, 0);
+    for (int64_t u = 0; u < ly.dh; ++u)
+      for (int j = 0; j < 2; ++j) {
+        const double v = get(3 + j, u);
+        if (es == 8) reinterpret_cast<double*>(b.data())[u * 2 + j] = v;
+        else reinterpret_cast<float*>(b.data())[u * 2 + j] = (float)v;
+      }
+    CUDA_TRY(cudaMalloc(&ly.bias, b.size()));
+    CUDA_TRY(cudaMemcpy(ly.bias, b.data(), b.size(), cudaMemcpyHostToDevice));
+    ly.wbytes += b.size();
+  }
+  ly.loaded = true;
+  cudaSetDevice(cur);
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_forward(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size, void* H,
+                         int64_t ldh, void* c_state, void* x_carry, void* stream) {
+  rnnb_status st = check_stack(h);
+  if (st != RNNB_OK) return st;
+  if (L < 1) return fail(RNNB_EINVAL, "seq_len must be >= 1");
+  if (block_size < 1) return fail(RNNB_EINVAL, "block_size must be >= 1");
+  if (!X || !H) return fail(RNNB_EINVAL, "null X or H");
+  if (ldx < h->layers[0].din) return fail(RNNB_EINVAL, "ldx smaller than d_in");
+  if (ldh < h->layers.back().dh) return fail(RNNB_EINVAL, "ldh smaller than d_h");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != h->device) CUDA_TRY(cudaSetDevice(h->device));
+  switch (h->mode) {
+    case RNNB_F64:
+      st = forward_t<double, double>(h, static_cast<const double*>(X), ldx, L, block_size,
+                                     static_cast<double*>(H), ldh, static_cast<double*>(c_state),
+                                     static_cast<double*>(x_carry), s);
+      break;
+    case RNNB_BF16:
+      st = forward_t<float, __nv_bfloat16>(h, static_cast<const float*>(X), ldx, L, block_size,
+                                           static_cast<float*>(H), ldh, static_cast<float*>(c_state),
+                                           static_cast<float*>(x_carry), s);
+      break;
+    default:
+      st = forward_t<float, float>(h, static_cast<const float*>(X), ldx, L, block_size, static_cast<float*>(H),
+                                   ldh, static_cast<float*>(c_state), static_cast<float*>(x_carry), s);
+  }
+  if (cur != h->device) cudaSetDevice(cur);
+  return st;
+}
+
+rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t block_size, void* H,
+                              void* c_state, void* x_carry, void* stream) {
+  rnnb_status st = check_stack(h);
+  if (st != RNNB_OK) return st;
+  if (L < 1) return fail(RNNB_EINVAL, "seq_len must be >= 1");
+  if (!X || !H) return fail(RNNB_EINVAL, "null X or H");
+  const size_t es = elem_size(h->mode);
+  const int64_t din = h->layers[0].din, dh = h->layers.back().dh;
+  int64_t csz = 0, xsz = 0;
+  for (auto& ly : h->layers) csz += ly.dh, xsz += ly.din;
+  const size_t xb = (size_t)L * din * es, hb = (size_t)L * dh * es;
+  const size_t sb = (size_t)(csz + xsz) * es;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (cur != h->device) CUDA_TRY(cudaSetDevice(h->device));
+  if (h->hx_bytes < xb + sb) {
+    if (h->hostX) cudaFree(h->hostX);
+    h->hostX = nullptr;
+    CUDA_TRY(cudaMalloc(&h->hostX, xb + sb));
+    h->hx_bytes = xb + sb;
+  }
+  if (h->hh_bytes < hb) {
+    if (h->hostH) cudaFree(h->hostH);
+    h->hostH = nullptr;
+    CUDA_TRY(cudaMalloc(&h->hostH, hb));
+    h->hh_bytes = hb;
+  }
+  char* dX = static_cast<char*>(h->hostX);
+  char* dC = dX + xb;
+  char* dXC = dC + csz * es;
+  CUDA_TRY(cudaMemcpyAsync(dX, X, xb, cudaMemcpyHostToDevice, s));
+  if (c_state) CUDA_TRY(cudaMemcpyAsync(dC, c_state, csz * es, cudaMemcpyHostToDevice, s));
+  if (x_carry) CUDA_TRY(cudaMemcpyAsync(dXC, x_carry, xsz * es, cudaMemcpyHostToDevice, s));
+  st = rnnb_forward(h, dX, din, L, block_size, h->hostH, dh, c_state ? dC : nullptr, x_carry ? dXC : nullptr, stream);
+  if (st == RNNB_OK) {
+    CUDA_TRY(cudaMemcpyAsync(H, h->hostH, hb, cudaMemcpyDeviceToHost, s));
+    if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
+    if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+  }
+  if (cur != h->device) cudaSetDevice(cur);
+  return st;
+}
+
+rnnb_status rnnb_gates(rnnb_stack_t h, int layer, const void* Xt, int64_t ldx, int64_t l, const void* x_carry,
+                       void* G, int64_t ldg, void* stream) {
+  rnnb_status st = check_stack(h);
+  if (st != RNNB_OK) return st;
+  if (layer < 0 || layer >= h->n_layers) return fail(RNNB_EINVAL, "layer index out of range");
+  if (l < 1) return fail(RNNB_EINVAL, "block must hold at least one step");
+  if (!Xt || !G) return fail(RNNB_EINVAL, "null X or G");
+  if (ldg < l) return fail(RNNB_EINVAL, "ldg smaller than block length");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const Layer& ly = h->layers[layer];
+  if (ldx < ly.din) return fail(RNNB_EINVAL, "ldx smaller than d_in");
+  switch (h->mode) {
+    case RNNB_F64:
+      return layer_launch<double, double>(h, layer, static_cast<const double*>(Xt), ldx, l, l, nullptr, 0, nullptr,
+                                          const_cast<double*>(static_cast<const double*>(x_carry)),
+                                          static_cast<double*>(G), ldg, s);
+    case RNNB_BF16:
+      return layer_launch<float, __nv_bfloat16>(h, layer, static_cast<const float*>(Xt), ldx, l, l, nullptr, 0,
+                                                nullptr, const_cast<float*>(static_cast<const float*>(x_carry)),
+                                                static_cast<float*>(G), ldg, s);
+    default:
+      return layer_launch<float, float>(h, layer, static_cast<const float*>(Xt), ldx, l, l, nullptr, 0, nullptr,
+                                        const_cast<float*>(static_cast<const float*>(x_carry)),
+                                        static_cast<float*>(G), ldg, s);
+  }
+}
+
+rnnb_status rnnb_sweep(const void* forget, const void* cand, const void* c_init, void* C, int64_t d, int64_t T,
+                       int dtype, void* stream) {
+  if (!forget || !cand || !c_init || !C) return fail(RNNB_EINVAL, "null argument");
+  if (d < 1 || T < 1) return fail(RNNB_EINVAL, "forget and candidate blocks must share one 2-d shape");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int bs = 128;
+  const int grid = (int)((d + bs - 1) / bs);
+  if (dtype == RNNB_DT_F64)
+    sweep_kernel<double><<<grid, bs, 0, s>>>(static_cast<const double*>(forget), static_cast<const double*>(cand),
+                                             static_cast<const double*>(c_init), static_cast<double*>(C), d, T);
+  else if (dtype == RNNB_DT_F32)
+    sweep_kernel<float><<<grid, bs, 0, s>>>(static_cast<const float*>(forget), static_cast<const float*>(cand),
+                                            static_cast<const float*>(c_init), static_cast<float*>(C), d, T);
+  else
+    return fail(RNNB_EINVAL, "dtype must be f32 or f64");
+  CUDA_TRY(cudaGetLastError());
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_finalize(int kind, const void* out_gate, const void* C, const void* Xb, void* H, int64_t d,
+                          int64_t T, int dtype, void* stream) {
+  if (kind != RNNB_SRU && kind != RNNB_QRNN) return fail(RNNB_EINVAL, "no blocked output path for this kind");
+  if (!out_gate || !C || !H) return fail(RNNB_EINVAL, "null argument");
+  if (kind == RNNB_SRU && !Xb) return fail(RNNB_EINVAL, "SRU output needs the raw input block");
+  if (d < 1 || T < 1) return fail(RNNB_EINVAL, "empty block");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t n = d * T;
+  const int bs = 256;
+  const int grid = (int)((n + bs - 1) / bs);
+  if (dtype == RNNB_DT_F64)
+    finalize_kernel<double><<<grid, bs, 0, s>>>(kind, static_cast<const double*>(out_gate),
+                                                static_cast<const double*>(C), static_cast<const double*>(Xb),
+                                                static_cast<double*>(H), n);
+  else if (dtype == RNNB_DT_F32)
+    finalize_kernel<float><<<grid, bs, 0, s>>>(kind, static_cast<const float*>(out_gate),
+                                               static_cast<const float*>(C), static_cast<const float*>(Xb),
+                                               static_cast<float*>(H), n);
+  else
+    return fail(RNNB_EINVAL, "dtype must be f32 or f64");
+  CUDA_TRY(cudaGetLastError());
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value) {
+  if (!h || !value) return fail(RNNB_EINVAL, "null argument");
+  if (what >= 2 && (layer < 0 || layer >= h->n_layers)) return fail(RNNB_EINVAL, "layer index out of range");
+  switch (what) {
+    case 0: {
+      int64_t b = 0;
+      for (auto& ly : h->layers) b += (int64_t)ly.wbytes;
+      *value = b;
+      return RNNB_OK;
+    }
+    case 1: *value = h->last_launches; return RNNB_OK;
+    case 2: *value = h->layers[layer].U; return RNNB_OK;
+    case 3: *value = h->layers[layer].last.wsmem ? 1 : 0; return RNNB_OK;
+    case 4: *value = h->layers[layer].grid; return RNNB_OK;
+    case 5: *value = (int64_t)h->layers[layer].last.smem; return RNNB_OK;
+    default: return fail(RNNB_EINVAL, "unknown query");
+  }
+}
+
+}  // extern "C"

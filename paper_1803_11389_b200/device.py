@@ -1,0 +1,181 @@
+"""Device-resident stack handle: weights uploaded once, forward on HBM tensors.
+
+This is the explicit-handle form of the drop-in API (the
+reference re-stacks weights on every ``run_blocked`` call and tests mutate
+weights between calls, so a fast path must take an explicit handle rather
+than cache by identity).  torch is only the allocator/stream plumbing here;
+all compute goes through ``librnnb.so`` (include/rnnb.h).
+"""
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .cells import CellKind, QRNN_FIELDS, SRU_FIELDS
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def kind_code(kind):
+    if isinstance(kind, CellKind):
+        if kind is CellKind.SRU:
+            return _lib.SRU
+        if kind is CellKind.QRNN:
+            return _lib.QRNN
+        raise ValueError("blocked execution covers SRU and QRNN; use lstm_run_precomputed for LSTM")
+    return kind_code(CellKind.parse(str(kind)))
+
+
+def canonical_mats(kind, layer):
+    fields = SRU_FIELDS if kind_code(kind) == _lib.SRU else QRNN_FIELDS
+    if isinstance(layer, (list, tuple)):
+        return list(layer)
+    if isinstance(layer, dict):
+        return [layer[f] for f in fields]
+    return [getattr(layer, f) for f in fields]
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class DeviceStack:
+    """Layers of one cell kind resident on one GPU.
+
+    mode: "f32" | "f64" (the reference precisions, FFMA/DFMA), "bf16"
+    (bf16 weights, x rounded to bf16 at the product, fp32 accumulate) or
+    "tf32" (weights and x rounded to tf32 at the product).
+    """
+
+    def __init__(self, kind, layers, mode="f32", device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _lib.RnnbError("CUDA is not available: the blocked path has no CPU fallback")
+        self.lib = _lib.load()
+        self.kind = kind_code(kind)
+        if mode not in _lib.MODES:
+            raise ValueError(f"mode must be one of {sorted(_lib.MODES)}")
+        self.mode = mode
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        mats = [canonical_mats(kind, lay) for lay in layers]
+        if not mats:
+            raise ValueError("a stack needs at least one layer")
+        self.d_in = [int(np.shape(m[0])[1]) for m in mats]
+        self.d_h = [int(np.shape(m[0])[0]) for m in mats]
+        n = len(mats)
+        din = (ctypes.c_int64 * n)(*self.d_in)
+        dh = (ctypes.c_int64 * n)(*self.d_h)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.rnnb_stack_create(ctypes.byref(h), self.kind, n, din, dh,
+                                              _lib.MODES[mode], self.device))
+        self._h = h
+        for li, m in enumerate(mats):
+            self.set_layer(li, m)
+
+    @property
+    def n_layers(self):
+        return len(self.d_h)
+
+    @property
+    def dtype(self):
+        torch = _torch()
+        return torch.float64 if self.mode == "f64" else torch.float32
+
+    @property
+    def np_dtype(self):
+        return np.float64 if self.mode == "f64" else np.float32
+
+    def set_layer(self, li, mats):
+        src = np.float64 if self.mode == "f64" else np.float32
+        arrs = [np.ascontiguousarray(np.asarray(m), dtype=src) for m in mats]
+        ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        dt = _lib.DT_F64 if src is np.float64 else _lib.DT_F32
+        _lib.check(self.lib.rnnb_stack_set_layer(self._h, li, ptrs, len(arrs), dt))
+
+    def _check_dev(self, t, name):
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.dtype != self.dtype:
+            raise ValueError(f"dtype mismatch: {t.dtype} vs {self.dtype}")
+        if t.dim() != 2 or t.stride(1) != 1:
+            raise ValueError(f"{name} must be a 2-d row-major tensor")
+
+    def forward(self, X, block_size, out=None, c_state=None, x_carry=None, stream=None):
+        """run_blocked on device tensors; X [L x d_in] -> [L x d_h]."""
+        torch = _torch()
+        self._check_dev(X, "X")
+        L = X.shape[0]
+        if X.shape[1] != self.d_in[0]:
+            raise ValueError(f"input must be [L x {self.d_in[0]}], got {tuple(X.shape)}")
+        if out is None:
+            out = torch.empty((L, self.d_h[-1]), dtype=self.dtype, device=X.device)
+        self._check_dev(out, "out")
+        cp = ctypes.c_void_p(c_state.data_ptr()) if c_state is not None else None
+        xp = ctypes.c_void_p(x_carry.data_ptr()) if x_carry is not None else None
+        _lib.check(self.lib.rnnb_forward(self._h, ctypes.c_void_p(X.data_ptr()), X.stride(0), L,
+                                         int(block_size), ctypes.c_void_p(out.data_ptr()),
+                                         out.stride(0), cp, xp, _stream_ptr(stream)))
+        return out
+
+    def forward_host(self, X, block_size, out=None, c_state=None, x_carry=None, stream=None):
+        """End-to-end call on HOST arrays: H2D, forward, D2H inside the C call."""
+        X = np.ascontiguousarray(X, dtype=self.np_dtype)
+        if X.ndim != 2 or X.shape[1] != self.d_in[0]:
+            raise ValueError(f"input must be [L x {self.d_in[0]}], got {X.shape}")
+        if out is None:
+            out = np.empty((X.shape[0], self.d_h[-1]), self.np_dtype)
+        cp = c_state.ctypes.data_as(ctypes.c_void_p) if c_state is not None else None
+        xp = x_carry.ctypes.data_as(ctypes.c_void_p) if x_carry is not None else None
+        _lib.check(self.lib.rnnb_forward_host(self._h, X.ctypes.data_as(ctypes.c_void_p), X.shape[0],
+                                              int(block_size), out.ctypes.data_as(ctypes.c_void_p),
+                                              cp, xp, _stream_ptr(stream)))
+        return out
+
+    def gates(self, layer, Xt, x_carry=None, stream=None):
+        """Activated gates [3, d_h, l] for one time-major block Xt [l x d_in]."""
+        torch = _torch()
+        self._check_dev(Xt, "Xt")
+        l = Xt.shape[0]
+        G = torch.empty((3, self.d_h[layer], l), dtype=self.dtype, device=Xt.device)
+        xp = ctypes.c_void_p(x_carry.data_ptr()) if x_carry is not None else None
+        _lib.check(self.lib.rnnb_gates(self._h, layer, ctypes.c_void_p(Xt.data_ptr()), Xt.stride(0), l, xp,
+                                       ctypes.c_void_p(G.data_ptr()), l, _stream_ptr(stream)))
+        return G
+
+    def query(self, what, layer=0):
+        v = ctypes.c_int64()
+        _lib.check(self.lib.rnnb_query(self._h, what, layer, ctypes.byref(v)))
+        return v.value
+
+    @property
+    def weight_bytes(self):
+        return self.query(0)
+
+    @property
+    def last_launches(self):
+        return self.query(1)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.rnnb_stack_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

@@ -1,0 +1,341 @@
+"""GPU parity: the CUDA path (through librnnb.so) against the oracle and the
+reference's own golden outputs.
+
+Tolerances (written per test):
+* fp32: normwise max|d|/max|ref| <= 1e-5 AND max|d| <= 1e-4
+  (the reference's ORACLE_TOLERANCE, bench.py:25);
+* f64: max|d| <= 1e-12;
+* TF32: <= 2e-3 normwise vs the fp32 oracle, <= 1e-5 vs the oracle on
+  tf32-rounded operands;
+* BF16: <= 2e-2 normwise vs the fp32 oracle, <= 1e-3 vs the oracle on
+  bf16-rounded weights and inputs.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+def normwise(a, ref):
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(np.asarray(a, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def assert_f32(a, ref):
+    d = float(np.max(np.abs(np.asarray(a, np.float64) - np.asarray(ref, np.float64))))
+    assert normwise(a, ref) <= 1e-5 and d <= 1e-4, (normwise(a, ref), d)
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1803_11389_b200 as P
+    return P
+
+
+def _ws(P, kind, layers, precision):
+    kind = P.CellKind.parse(kind)
+    cls = P.SruWeights if kind is P.CellKind.SRU else P.QrnnWeights
+    return P.WeightSet(kind, precision, [cls(*[np.ascontiguousarray(m) for m in lay]) for lay in layers])
+
+
+def _cfg(P, kind, d, n_layers, precision):
+    return P.RnnConfig(P.CellKind.parse(kind), d, d, n_layers=n_layers, precision=precision)
+
+
+def _cases():
+    with open(os.path.join(GOLDEN, "blocked_cases.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("case", _cases(), ids=lambda c: f"{c['kind']}-{c['precision']}-d{c['d']}-L{c['L']}-n{c['n_layers']}")
+def test_run_blocked_matches_reference_fixtures(P, oracle, case):
+    g = np.load(os.path.join(GOLDEN, "blocked_cases.npz"))
+    prec = case["precision"]
+    dt = np.float32 if prec == "f32" else np.float64
+    layers = oracle.generate_layers(case["kind"], case["d"], case["d"], case["n_layers"], case["wseed"], dt)
+    X = oracle.generate_sequence(case["L"], case["d"], case["xseed"], dt)
+    cfg = _cfg(P, case["kind"], case["d"], case["n_layers"], prec)
+    ws = _ws(P, case["kind"], layers, prec)
+    n = case["case"]
+    for T in case["T_b"]:
+        H, cs, xcs = P.run_blocked(cfg, ws, X, T, return_state=True)
+        assert H.dtype == dt and H.shape == (case["L"], case["d"])
+        ref = g[f"c{n}_T{T}_H"]
+        if prec == "f32":
+            assert_f32(H, ref)
+            assert_f32(np.stack(cs), g[f"c{n}_T{T}_c"])
+        else:
+            assert np.max(np.abs(H - ref)) <= 1e-12
+            assert np.max(np.abs(np.stack(cs) - g[f"c{n}_T{T}_c"])) <= 1e-12
+        # and against the stepwise oracle of the reference (bench.verify)
+        step = g[f"c{n}_stepwise"]
+        assert np.max(np.abs(H - step)) <= (1e-4 if prec == "f32" else 1e-9)
+
+
+@pytest.mark.parametrize("kind", ["sru", "qrnn"])
+def test_d2_golden_vectors_on_gpu(P, kind):
+    with open(os.path.join(GOLDEN, "cells_d2.json")) as f:
+        g = json.load(f)[kind]
+    fields = ("w_cand", "w_forget", "w_highway", "b_forget", "b_highway") if kind == "sru" else \
+        ("w_cand", "w_cand_prev", "w_forget", "w_forget_prev", "w_out", "w_out_prev")
+    layer = [np.array(g["weights"][f], np.float64) for f in fields]
+    X = np.array(g["X"], np.float64)
+    cfg = _cfg(P, kind, 2, 1, "f64")
+    for T in (1, 2, 3):
+        H, cs, _ = P.run_blocked(cfg, _ws(P, kind, [layer], "f64"), X, T, return_state=True)
+        assert np.max(np.abs(H - np.array(g["H"]))) < 1e-12
+        assert np.max(np.abs(cs[0] - np.array(g["C"][-1]))) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["sru", "qrnn"])
+@pytest.mark.parametrize("d", [3, 40, 256])
+def test_block_size_sweep_vs_oracle(P, oracle, kind, d):
+    """Every T_b incl. remainders, T_b > L and non-power-of-2 widths."""
+    L = 150
+    layers = oracle.generate_layers(kind, d, d, 1, 100 + d, np.float32)
+    X = np.random.default_rng(d).standard_normal((L, d)).astype(np.float32)
+    cfg = _cfg(P, kind, d, 1, "f32")
+    ws = _ws(P, kind, layers, "f32")
+    for T in (1, 2, 3, 4, 5, 8, 13, 16, 17, 32, 64, 128, 200):
+        ref, cref, _ = oracle.run_blocked(kind, layers, X, T, return_state=True)
+        H, cs, xcs = P.run_blocked(cfg, ws, X, T, return_state=True)
+        assert_f32(H, ref)
+        assert_f32(cs[0], cref[0])
+        if kind == "qrnn":
+            assert np.array_equal(xcs[0], X[-1])
+
+
+def test_single_step_and_tiny_sequences(P, oracle):
+    for kind in ("sru", "qrnn"):
+        layers = oracle.generate_layers(kind, 64, 64, 1, 3, np.float32)
+        for L in (1, 2, 7):
+            X = oracle.generate_sequence(L, 64, 4, np.float32)
+            ref = oracle.run_stepwise(kind, layers, X)
+            for T in (1, 4, 32):
+                assert_f32(P.run_blocked(_cfg(P, kind, 64, 1, "f32"), _ws(P, kind, layers, "f32"), X, T), ref)
+
+
+def test_multilayer_stacks_vs_oracle(P, oracle):
+    for kind, d, nl in (("sru", 256, 3), ("qrnn", 192, 4)):
+        layers = oracle.generate_layers(kind, d, d, nl, 11, np.float32)
+        X = np.random.default_rng(2).standard_normal((300, d)).astype(np.float32)
+        for T in (1, 8, 32):
+            ref = oracle.run_blocked(kind, layers, X, T)
+            assert_f32(P.run_blocked(_cfg(P, kind, d, nl, "f32"), _ws(P, kind, layers, "f32"), X, T), ref)
+
+
+def test_baseline_cfg1_full(P, oracle):
+    """BASELINE cfg1 at full size against the reference's own outputs."""
+    from paper_1803_11389_b200 import workloads
+    g = np.load(os.path.join(GOLDEN, "baseline_cfg.npz"))
+    w = workloads.make("cfg1")
+    cfg = _cfg(P, "sru", 512, 1, "f32")
+    ws = P.WeightSet(P.CellKind.SRU, "f32", w.layers)
+    for T in (1, 4, 16):
+        H, cs, _ = P.run_blocked(cfg, ws, w.X, T, return_state=True)
+        assert_f32(cs[0], g[f"cfg1_T{T}_c"])
+        assert_f32(H, g["cfg1_T16_H"])
+
+
+def test_baseline_cfg2_full(P, oracle):
+    """BASELINE cfg2 (QRNN 1024, L=2048) at full size: reference row
+    subsample + c_T, plus the oracle over the whole output at every T_b."""
+    import torch
+    from paper_1803_11389_b200 import workloads
+    g = np.load(os.path.join(GOLDEN, "baseline_cfg.npz"))
+    w = workloads.make("cfg2")
+    layers = [lay.mats() for lay in w.layers]
+    st = P.DeviceStack(P.CellKind.QRNN, w.layers, mode="f32")
+    Xd = torch.from_numpy(w.X).cuda()
+    for T in w.block_sizes:
+        c = torch.zeros(1024, dtype=torch.float32, device="cuda")
+        H = st.forward(Xd, T, c_state=c).cpu().numpy()
+        if T == 32:
+            assert_f32(H[g["cfg2_T32_rows"]], g["cfg2_T32_Hrows"])
+            assert_f32(c.cpu().numpy(), g["cfg2_T32_c"])
+        ref, cref, _ = oracle.run_blocked("qrnn", layers, w.X, T, return_state=True)
+        assert_f32(H, ref)
+        assert_f32(c.cpu().numpy(), cref[0])
+    st.close()
+
+
+def test_streaming_state_carry_equals_whole_sequence(P, oracle):
+    """c and x_carry in/out across calls: two half-sequence calls on a block
+    boundary reproduce the whole-sequence call bit for bit."""
+    import torch
+    for kind in ("sru", "qrnn"):
+        layers = oracle.generate_layers(kind, 128, 128, 2, 21, np.float32)
+        X = np.random.default_rng(3).standard_normal((256, 128)).astype(np.float32)
+        st = P.DeviceStack(kind, layers, mode="f32")
+        Xd = torch.from_numpy(X).cuda()
+        whole = st.forward(Xd, 16).cpu().numpy()
+        c = torch.zeros(256, device="cuda")
+        xc = torch.zeros(256, device="cuda")
+        a = st.forward(Xd[:96].contiguous(), 16, c_state=c, x_carry=xc).cpu().numpy()
+        b = st.forward(Xd[96:].contiguous(), 16, c_state=c, x_carry=xc).cpu().numpy()
+        assert np.concatenate([a, b]).tobytes() == whole.tobytes()
+        st.close()
+
+
+def test_strided_device_input(P, oracle):
+    import torch
+    layers = oracle.generate_layers("qrnn", 96, 96, 1, 5, np.float32)
+    X = np.random.default_rng(4).standard_normal((64, 96)).astype(np.float32)
+    st = P.DeviceStack("qrnn", layers)
+    big = torch.zeros((64, 128), device="cuda")
+    big[:, :96] = torch.from_numpy(X).cuda()
+    a = st.forward(big[:, :96], 8).cpu().numpy()
+    b = st.forward(torch.from_numpy(X).cuda(), 8).cpu().numpy()
+    assert a.tobytes() == b.tobytes()
+    st.close()
+
+
+def test_host_e2e_matches_device(P, oracle):
+    import torch
+    layers = oracle.generate_layers("sru", 512, 512, 1, 6, np.float32)
+    X = np.random.default_rng(5).standard_normal((200, 512)).astype(np.float32)
+    st = P.DeviceStack("sru", layers)
+    a = st.forward_host(X, 16)
+    b = st.forward(torch.from_numpy(X).cuda(), 16).cpu().numpy()
+    assert a.tobytes() == b.tobytes()
+    st.close()
+
+
+# ---------------------------------------------------------------------------
+# unit-level ops (blocked.py:123-193)
+
+
+def _sig(z):
+    return 0.5 * (1.0 + np.tanh(0.5 * z))
+
+
+def test_precompute_gates_sru(P, oracle):
+    layers = oracle.generate_layers("sru", 64, 64, 1, 8, np.float64)
+    lay = layers[0]
+    w = P.SruWeights(*lay)
+    Xb = np.ascontiguousarray(oracle.generate_sequence(16, 64, 9, np.float64).T)
+    g = P.precompute_gates_sru(w, Xb)
+    assert np.max(np.abs(g.cand - lay[0] @ Xb)) <= 1e-12
+    assert np.max(np.abs(g.forget - _sig(lay[1] @ Xb + lay[3][:, None]))) <= 1e-12
+    assert np.max(np.abs(g.out_gate - _sig(lay[2] @ Xb + lay[4][:, None]))) <= 1e-12
+    # zero weights: cand 0, forget sigma(b), highway 0.5 (test_blocked.py:105-118 property)
+    z = np.zeros((3, 3))
+    w0 = P.SruWeights(z, z.copy(), z.copy(), np.array([0.3, -0.1, 0.0]), np.zeros(3))
+    g0 = P.precompute_gates_sru(w0, np.ones((3, 4)))
+    assert np.allclose(g0.cand, 0.0) and (g0.out_gate == 0.5).all()
+    assert np.max(np.abs(g0.forget - _sig(np.array([0.3, -0.1, 0.0]))[:, None])) <= 1e-15
+
+
+def test_precompute_gates_qrnn_carry_and_ablation(P, oracle):
+    lay = oracle.generate_layers("qrnn", 48, 48, 1, 10, np.float64)[0]
+    w = P.QrnnWeights(*lay)
+    X = oracle.generate_sequence(12, 48, 11, np.float64)
+    b1, b2 = np.ascontiguousarray(X[:5].T), np.ascontiguousarray(X[5:].T)
+    g2 = P.precompute_gates_qrnn(w, b2, np.ascontiguousarray(b1[:, -1]))
+    xprev = np.concatenate([b1[:, -1:], b2[:, :-1]], axis=1)
+    assert np.max(np.abs(g2.cand - np.tanh(lay[0] @ b2 + lay[1] @ xprev))) <= 1e-12
+    assert np.max(np.abs(g2.forget - _sig(lay[2] @ b2 + lay[3] @ xprev))) <= 1e-12
+    assert np.max(np.abs(g2.out_gate - _sig(lay[4] @ b2 + lay[5] @ xprev))) <= 1e-12
+    for m in (1, 3, 5):
+        lay[m][:] = 0.0
+    w = P.QrnnWeights(*lay)
+    a = P.precompute_gates_qrnn(w, b2, np.zeros(48))
+    b = P.precompute_gates_qrnn(w, b2, np.full(48, 9.0))
+    assert (a.cand == b.cand).all() and (a.forget == b.forget).all()
+
+
+def test_sweep_and_finalize_known_answers(P):
+    C = P.recurrence_sweep(np.array([[0.5, 0.5]]), np.array([[1.0, 1.0]]), np.zeros(1))
+    assert C.tolist() == [[0.5, 0.75]]
+    d, T = 4, 6
+    Xh = np.random.default_rng(0).uniform(-1, 1, (d, T))
+    c0 = np.array([0.1, -0.2, 0.3, -0.4])
+    assert (P.recurrence_sweep(np.ones((d, T)), Xh, c0) == c0[:, None]).all()
+    assert (P.recurrence_sweep(np.zeros((d, T)), Xh, np.ones(d)) == Xh).all()
+    Cm = np.random.default_rng(2).uniform(-1, 1, (3, 5))
+    gq = P.GateBlock(cand=np.zeros_like(Cm), forget=np.zeros_like(Cm), out_gate=np.ones_like(Cm))
+    assert np.max(np.abs(P.finalize_outputs(P.CellKind.QRNN, gq, Cm) - np.tanh(Cm))) <= 1e-15
+    Xb = np.random.default_rng(4).uniform(-1, 1, (3, 5))
+    gs = P.GateBlock(cand=np.zeros_like(Cm), forget=np.zeros_like(Cm), out_gate=np.zeros_like(Cm))
+    assert (P.finalize_outputs(P.CellKind.SRU, gs, Cm, Xb) == Xb).all()
+    with pytest.raises(ValueError):
+        P.finalize_outputs(P.CellKind.SRU, gs, Cm)
+    with pytest.raises(ValueError):
+        P.recurrence_sweep(np.zeros((2, 3)), np.zeros((2, 4)), np.zeros(2))
+
+
+def test_blocked_errors_match_reference(P, oracle):
+    lay = oracle.generate_layers("sru", 8, 8, 1, 1, np.float32)
+    cfg = _cfg(P, "sru", 8, 1, "f32")
+    ws = _ws(P, "sru", lay, "f32")
+    X = np.zeros((4, 8), np.float32)
+    with pytest.raises(ValueError):
+        P.run_blocked(cfg, ws, np.zeros((4, 9), np.float32), 2)
+    with pytest.raises(ValueError):
+        P.run_blocked(cfg, ws, X, 0)
+    with pytest.raises(ValueError):
+        P.run_blocked(cfg, ws, X, 2, kernel="bogus")
+    with pytest.raises(ValueError, match="dtype mismatch"):
+        P.run_blocked(cfg, ws, X.astype(np.float64), 2)
+    with pytest.raises(ValueError):
+        P.run_blocked(P.RnnConfig(P.CellKind.LSTM, 8, 8), ws, X, 2)
+
+
+# ---------------------------------------------------------------------------
+# tensor-core numerics modes
+
+
+def _round_tf32(a):
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x1000) & 0xFFFFE000).astype(np.uint32)
+    return u.view(np.float32)
+
+
+def _round_bf16(a):
+    u = np.ascontiguousarray(a, np.float32).view(np.uint32).astype(np.uint64)
+    u = ((u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000).astype(np.uint32)
+    return u.view(np.float32)
+
+
+@pytest.mark.parametrize("kind", ["sru", "qrnn"])
+@pytest.mark.parametrize("mode", ["tf32", "bf16"])
+def test_reduced_precision_modes(P, oracle, kind, mode):
+    import torch
+    d = 512
+    layers = oracle.generate_layers(kind, d, d, 2, 31, np.float32)
+    X = np.random.default_rng(7).standard_normal((256, d)).astype(np.float32)
+    st = P.DeviceStack(kind, layers, mode=mode)
+    rnd = _round_tf32 if mode == "tf32" else _round_bf16
+    for T in (1, 16, 32):
+        H = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
+        ref = oracle.run_blocked(kind, layers, X, T)
+        assert normwise(H, ref) <= (2e-3 if mode == "tf32" else 2e-2)
+        # vs the oracle fed rounded weights and rounded MMA operands, layer by layer
+        inp = X
+        for lay in layers:
+            rl = [rnd(m) if m.ndim == 2 else m for m in lay]
+            xr = rnd(inp)
+            if kind == "sru":
+                # highway term uses the unrounded input; emulate by correcting
+                out_r = oracle.run_blocked(kind, [rl], xr, T)
+                out_u = _sru_highway_fix(oracle, rl, xr, inp, T)
+                inp = out_u
+            else:
+                inp = oracle.run_blocked(kind, [rl], xr, T)
+        assert normwise(H, inp) <= (1e-5 if mode == "tf32" else 1e-3)
+    st.close()
+
+
+def _sru_highway_fix(oracle, rl, xr, x, T):
+    """SRU with products on rounded x but the (1-r) x highway on the raw x."""
+    import numpy as _np
+    H = oracle.run_blocked("sru", [rl], xr, T)
+    # H = r tanh c + (1-r) xr  ->  replace xr by x: add (1-r)(x - xr)
+    r = 0.5 * (1.0 + _np.tanh(0.5 * (xr.astype(_np.float64) @ rl[2].T.astype(_np.float64) + rl[4])))
+    return (H + (1.0 - r) * (x.astype(_np.float64) - xr.astype(_np.float64))).astype(_np.float32)
