@@ -129,12 +129,18 @@ FAST_DEFINE(double, f64)
                 g[i * l + t] = (T)0.5 * ((T)1 + TANH((T)0.5 * (g[i * l + t] + bi)));       \
         }                                                                                  \
     }                                                                                      \
-    ORC_CLONES void orc_tap_act_fast_##SFX(T *g, const T *tmp, int64_t n, int is_tanh)     \
+    /* row-parallel so the SIMD/remainder split of every row is independent of   */ \
+    /* the thread count (results must not depend on it, kernels.py:101-110)       */ \
+    ORC_CLONES void orc_tap_act_fast_##SFX(T *g, const T *tmp, int64_t dh, int64_t l,      \
+                                           int is_tanh)                                    \
     {                                                                                      \
-        _Pragma("omp parallel for simd schedule(static) if(n > 2048)")                    \
-        for (int64_t e = 0; e < n; ++e) {                                                  \
-            T z = g[e] + tmp[e];                                                           \
-            g[e] = is_tanh ? TANH(z) : (T)0.5 * ((T)1 + TANH((T)0.5 * z));                 \
+        _Pragma("omp parallel for schedule(static) if(dh * l > 2048)")                    \
+        for (int64_t i = 0; i < dh; ++i) {                                                 \
+            _Pragma("omp simd")                                                            \
+            for (int64_t t = 0; t < l; ++t) {                                              \
+                T z = g[i * l + t] + tmp[i * l + t];                                       \
+                g[i * l + t] = is_tanh ? TANH(z) : (T)0.5 * ((T)1 + TANH((T)0.5 * z));     \
+            }                                                                              \
         }                                                                                  \
     }                                                                                      \
     ORC_CLONES void orc_sweep_out_fast_##SFX(int sru, const T *g0, const T *g1,            \

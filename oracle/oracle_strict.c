@@ -43,8 +43,8 @@ void orc_gemm_fast_f64(const double *A, const double *Bt, double *C, int64_t m, 
 void orc_set_threads(int n);
 void orc_sig_bias_fast_f32(float *g, const float *b, int64_t dh, int64_t l);
 void orc_sig_bias_fast_f64(double *g, const double *b, int64_t dh, int64_t l);
-void orc_tap_act_fast_f32(float *g, const float *tmp, int64_t n, int is_tanh);
-void orc_tap_act_fast_f64(double *g, const double *tmp, int64_t n, int is_tanh);
+void orc_tap_act_fast_f32(float *g, const float *tmp, int64_t dh, int64_t l, int is_tanh);
+void orc_tap_act_fast_f64(double *g, const double *tmp, int64_t dh, int64_t l, int is_tanh);
 void orc_sweep_out_fast_f32(int sru, const float *g0, const float *g1, const float *g2, const float *Xb,
                             float *c, float *Hout, int64_t s, int64_t dh, int64_t l);
 void orc_sweep_out_fast_f64(int sru, const double *g0, const double *g1, const double *g2, const double *Xb,
@@ -163,7 +163,7 @@ void orc_uniform(const uint64_t *raw, double *out, int64_t n)
                     gemm_##SFX(mats[2 * g], Xb, Xbt, gs[g], dh, din, l, kernel);           \
                     gemm_##SFX(mats[2 * g + 1], Xp, Xpt, tmp, dh, din, l, kernel);         \
                     if (kernel == ORC_KERNEL_FAST) {                                       \
-                        orc_tap_act_fast_##SFX(gs[g], tmp, dh * l, g == 0);                \
+                        orc_tap_act_fast_##SFX(gs[g], tmp, dh, l, g == 0);                    \
                         continue;                                                          \
                     }                                                                      \
                     for (int64_t e = 0; e < dh * l; ++e) {                                 \
