@@ -308,7 +308,9 @@ def _round_bf16(a):
 def test_reduced_precision_modes(P, oracle, kind, mode):
     import torch
     d = 512
-    layers = oracle.generate_layers(kind, d, d, 2, 31, np.float32)
+    # the "vs rounded oracle" bound is per layer: for a stack, ulp differences in
+    # layer-1 outputs flip tf32/bf16 roundings of layer-2 operands
+    layers = oracle.generate_layers(kind, d, d, 1, 31, np.float32)
     X = np.random.default_rng(7).standard_normal((256, d)).astype(np.float32)
     st = P.DeviceStack(kind, layers, mode=mode)
     rnd = _round_tf32 if mode == "tf32" else _round_bf16
