@@ -271,7 +271,9 @@ def run_ours(args, rank, world, local_rank):
                    "l2": "flushed before every timed step (256 MB write)",
                    "weights_smem_resident": resident,
                    "units_per_cta": [st.query(2, li) for li in range(st.n_layers)],
-                   "grid": [st.query(4, li) for li in range(st.n_layers)]},
+                   "grid": [st.query(4, li) for li in range(st.n_layers)],
+                   "kernel": ["ffma_ws (TMA producer + mbarrier ring + epilogue warp)" if st.query(6, li)
+                              else "ffma_layer" for li in range(st.n_layers)]},
         "e2e": e2e,
         "gpu_launches": int(head["launches"] * args.steps),
         "roofline": roof,

@@ -2,7 +2,8 @@
 // T_b, the shared-memory plan (weights resident or streamed from L2) and
 // instantiates the kernel for one (accumulate, weight) type pair.
 #pragma once
-#include "ffma_layer.cuh"
+#include <cstdlib>
+#include "ffma_ws.cuh"
 
 namespace rnnb {
 
@@ -31,9 +32,74 @@ static cudaError_t launch_one(const LayerArgs<TA, TW>& a, int grid, size_t smem,
 struct FfmaPlan {
   int nt = 1;
   bool wsmem = false;
+  bool ws = false;  // warp-specialised TMA/mbarrier kernel (ffma_ws.cuh)
   int kc = 0;
   size_t smem = 0;
 };
+
+template <typename TA, typename TW, int CELL, int NT, int U, int XR>
+static cudaError_t launch_ws_xr(const LayerArgs<TA, TW>& a, const CUtensorMap& tm, int grid, size_t smem,
+                                cudaStream_t s) {
+  auto k = ffma_ws_kernel<TA, TW, CELL, NT, U, XR>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  k<<<grid, kWsThreads, smem, s>>>(a, tm);
+  return cudaGetLastError();
+}
+
+// x rounding is a template parameter of the warp-specialised kernel
+template <typename TA, typename TW, int CELL, int NT, int U>
+static cudaError_t launch_ws(const LayerArgs<TA, TW>& a, const CUtensorMap& tm, int grid, size_t smem,
+                             cudaStream_t s) {
+  if (sizeof(TW) == 2) return launch_ws_xr<TA, TW, CELL, NT, U, XR_BF16>(a, tm, grid, smem, s);
+  if (sizeof(TA) == 4 && a.xround == XR_TF32) return launch_ws_xr<TA, TW, CELL, NT, U, XR_TF32>(a, tm, grid, smem, s);
+  return launch_ws_xr<TA, TW, CELL, NT, U, XR_NONE>(a, tm, grid, smem, s);
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+// 2-D map over the layer input X [L x D] (row stride ldx); box = NT+1 rows x
+// (KC + PADV) columns so TMA writes rows at the padded smem pitch.
+template <typename TA>
+static bool make_x_map(CUtensorMap* tm, const TA* X, int64_t D, int64_t L, int64_t ldx, int box_cols, int box_rows) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {(cuuint64_t)D, (cuuint64_t)L};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ldx * (int64_t)sizeof(TA))};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = enc(tm, sizeof(TA) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                   const_cast<TA*>(X), gdim, gstride, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+// The warp-specialised kernel needs 16-byte rows it can bulk-copy.
+template <typename TA, typename TW>
+static bool ws_eligible(const LayerArgs<TA, TW>& a) {
+  const int KV = 16 / (int)sizeof(TA);
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return a.G == nullptr && a.D == a.Dp && (a.ldx % KV) == 0 && al(a.X) &&
+         (a.xcarry == nullptr || al(a.xcarry)) && getenv("RNNB_NO_WS") == nullptr;
+}
 
 template <typename TA, typename TW, int CELL, int NT, int U>
 static FfmaPlan plan_nt(int Dp, bool allow_wsmem) {
@@ -56,6 +122,28 @@ static FfmaPlan plan_nt(int Dp, bool allow_wsmem) {
 
 template <typename TA, typename TW, int CELL, int NT, int U>
 static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaStream_t s, FfmaPlan* out) {
+  if (allow_wsmem && ws_eligible(a)) {
+    using WC = WsCfg<TA, TW, CELL, NT, U>;
+    constexpr int BWMAX = 512 / (int)sizeof(TA);  // 512-byte TMA boxes
+    do {
+      // one k-vector per consumer lane per tap per chunk (see ffma_ws.cuh)
+      int kc = WC::KL * WC::KV;
+      if (kc > a.Dp) kc = a.Dp;
+      int bw = WC::KV;  // power-of-two box width >= the chunk, capped at 512 bytes
+      while (bw < kc && bw < BWMAX) bw <<= 1;
+      const int nbox = (kc + bw - 1) / bw;
+      size_t sm = ws_smem_bytes<TA, TW, CELL, NT, U>(a.Dp, nbox * bw, bw);
+      if (sm > kMaxSmem) break;
+      CUtensorMap tm;
+      if (!make_x_map<TA>(&tm, a.X, a.D, a.L, a.ldx, bw + WC::PADV, NT + 1)) break;
+      FfmaPlan p;
+      p.nt = NT; p.wsmem = true; p.ws = true; p.kc = kc; p.smem = sm;
+      a.KC = kc;
+      a.KCB = bw;
+      if (out) *out = p;
+      return launch_ws<TA, TW, CELL, NT, U>(a, tm, grid, sm, s);
+    } while (0);
+  }
   FfmaPlan p = plan_nt<TA, TW, CELL, NT, U>(a.Dp, allow_wsmem);
   a.KC = p.kc;
   if (out) *out = p;

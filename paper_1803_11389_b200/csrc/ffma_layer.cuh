@@ -48,7 +48,9 @@ struct LayerArgs {
   int T_b;
   int D, Dp, H;
   int KC;              // K-chunk (elements per tap) staged per pipeline step
+  int KCB;             // TMA box width inside a chunk (ws kernel)
   int xround;          // XRound
+  int dbg;             // debug switches (RNNB_DEBUG): bit0 consumers skip the x-ready wait
 };
 
 constexpr int kThreads = 256;

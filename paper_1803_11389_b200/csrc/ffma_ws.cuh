@@ -1,0 +1,359 @@
+// Warp-specialised fused blocked SRU/QRNN layer kernel (FFMA pipe), v2.
+//
+// Same math and reference mapping as ffma_layer.cuh (rnnblock blocked.py:
+// 123-193, 221-268), re-organised for B200:
+//   * weights for the CTA's U units live in shared memory for the whole
+//     sequence in a k-vector-major layout Ws[kv][Rs][KV], so the 3U rows of
+//     one k-vector sit at compile-time offsets (one address per item);
+//   * warp 8 is a TMA producer: cp.async.bulk copies of x-row chunks into a
+//     STAGES-deep ring guarded by full/empty mbarriers (no __syncthreads in
+//     the main loop);
+//   * warps 0-7 are FFMA consumers (K split across warps and lanes);
+//   * warp 9 is the epilogue: cross-warp sums, bias + activations, the
+//     sequential c-scan, the output mix and the h stores of pass p run
+//     while the consumers already multiply pass p+1.
+// Requirements (checked on the host): D % 8 == 0, 16-byte aligned X /
+// x_carry rows, ldx % 4 == 0 and the weight slice fits in shared memory.
+#pragma once
+#include <cuda.h>  // CUtensorMap (type only; encoded via the runtime's driver entry point)
+
+#include "ffma_layer.cuh"
+
+namespace rnnb {
+
+constexpr int kWsComputeWarps = 16;
+constexpr int kWsEpiWarps = 4;
+constexpr int kWsEpiThreads = kWsEpiWarps * 32;
+constexpr int kWsThreads = (kWsComputeWarps + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group
+
+// named barrier 1 over the epilogue warpgroup only
+__device__ __forceinline__ void epi_bar_sync() {
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kWsEpiThreads) : "memory");
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}\n" ::"r"(
+                   smem_u32(bar)),
+               "r"(tx)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 2-D TMA tile load (tensor map in param space), completion on `bar`
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Consumer mapping: kWsComputeWarps = KG k-groups x RG row-groups.  A warp
+// owns RH = ceil(R/RG) rows over its k-group's share of K; inside the warp
+// LANES_T lanes split the NT columns (CT columns each) and LANES_K lanes
+// split K.  Two columns per lane whenever NT >= 2 keeps the weight LDS
+// amortised over 2*KV FMAs; the x LDS over RH*KV FMAs.
+template <typename TA, typename TW, int CELL, int NT, int U>
+struct WsCfg {
+  static constexpr int KV = 16 / (int)sizeof(TA);
+  static constexpr int TAPS = CELL == QRNN ? 2 : 1;
+  static constexpr int R = 3 * U;
+  static constexpr int KG = 8, RG = 2;
+  static_assert(KG * RG == kWsComputeWarps, "consumer warp split");
+  static constexpr int RH = (R + RG - 1) / RG;
+  static constexpr int Rpad = RH * RG;
+  // smem row count per k-vector: odd so consecutive kv (lanes kq) hit distinct
+  // 16-byte bank groups; rows [R, Rpad) read garbage that is never used
+  static constexpr int Rs = (R % 2) ? R : R + 1;
+  static constexpr int LANES_T = NT >= 2 ? NT / 2 : 1;
+  static constexpr int CT = NT / LANES_T;
+  static constexpr int LANES_K = 32 / LANES_T;
+  static constexpr int KL = KG * LANES_K;
+  // padded x row pitch: each 8-lane phase (LANES_T rows x 8/LANES_T k-vectors)
+  // must hit 8 distinct 16-byte bank groups; one row needs no padding
+  static constexpr int PADV = LANES_T == 1 ? 0 : KV * (LANES_T >= 8 ? 1 : 8 / LANES_T);
+  static constexpr int STAGES = 4;
+};
+
+// x chunk of KC columns = KC/BW TMA boxes of [NT+1 rows x (BW + PADV) cols],
+// each box at a 128-byte aligned stride inside the stage buffer
+template <typename TA, typename TW, int CELL, int NT, int U>
+__host__ __device__ inline size_t ws_box_elems(int BW) {
+  using C = WsCfg<TA, TW, CELL, NT, U>;
+  return align_up((size_t)(NT + 1) * (BW + C::PADV), 128 / sizeof(TA));
+}
+
+template <typename TA, typename TW, int CELL, int NT, int U>
+__host__ __device__ inline size_t ws_smem_bytes(int Dp, int KC, int BW) {
+  using C = WsCfg<TA, TW, CELL, NT, U>;
+  size_t off = align_up((size_t)C::TAPS * Dp / C::KV * C::Rs * C::KV * sizeof(TW) + 16 * C::RG, 128);
+  off += (size_t)C::STAGES * (KC / BW) * ws_box_elems<TA, TW, CELL, NT, U>(BW) * sizeof(TA);
+  off += (size_t)C::KG * C::Rpad * NT * sizeof(TA);
+  off += (size_t)3 * U * NT * sizeof(TA);
+  off = align_up(off, 8);
+  off += (2 * C::STAGES + 2) * sizeof(uint64_t);
+  return off;
+}
+
+template <typename TA, typename TW, int CELL, int NT, int U, int XR>
+__global__ void __launch_bounds__(kWsThreads, 1)
+    ffma_ws_kernel(LayerArgs<TA, TW> a, const __grid_constant__ CUtensorMap tmx) {
+  using C = WsCfg<TA, TW, CELL, NT, U>;
+  constexpr int KV = C::KV, TAPS = C::TAPS, R = C::R, Rs = C::Rs, KG = C::KG, RH = C::RH, Rpad = C::Rpad;
+  constexpr int LANES_T = C::LANES_T, CT = C::CT, LANES_K = C::LANES_K, KL = C::KL;
+  constexpr int STAGES = C::STAGES;
+  const int KC = a.KC;
+  const int BW = a.KCB;                  // TMA box width (columns)
+  const int BXS = BW + C::PADV;          // padded row pitch inside a box
+  const int LVPB = __ffs(BW / KV) - 1;   // log2(k-vectors per box); BW is a power of 2
+  const int MVPB = BW / KV - 1;
+  const int BOXS = (int)ws_box_elems<TA, TW, CELL, NT, U>(BW);
+  const int Dp = a.Dp;
+  const int Kv = TAPS * Dp / KV;  // k-vectors per row
+
+  extern __shared__ __align__(128) unsigned char smem[];
+  size_t off = 0;
+  TW* Ws = reinterpret_cast<TW*>(smem);
+  off = align_up((size_t)Kv * Rs * KV * sizeof(TW) + 16 * C::RG, 128);  // TMA dst: 128-B aligned
+  TA* Xr = reinterpret_cast<TA*>(smem + off);
+  const size_t stage_bytes = (size_t)((KC + BW - 1) / BW) * BOXS * sizeof(TA);
+  off += (size_t)STAGES * stage_bytes;
+  TA* red = reinterpret_cast<TA*>(smem + off);
+  off += (size_t)KG * Rpad * NT * sizeof(TA);
+  TA* gate = reinterpret_cast<TA*>(smem + off);
+  off += (size_t)3 * U * NT * sizeof(TA);
+  off = align_up(off, 8);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
+  uint64_t* empty = full + STAGES;
+  uint64_t* redfull = empty + STAGES;
+  uint64_t* redempty = redfull + 1;
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int u0 = blockIdx.x * U;
+  const TW* Wg = a.W + (size_t)u0 * 3 * TAPS * Dp;
+
+  // weights -> Ws[kv][r][:], once per launch (rows of Wg are [R][Kp])
+  {
+    constexpr int VB = KV * (int)sizeof(TW);  // bytes per (kv, r) vector
+    const int nvec = R * Kv;
+    for (int i = tid; i < nvec; i += kWsThreads) {
+      const int r = i / Kv, kv = i - (i / Kv) * Kv;
+      char* dst = reinterpret_cast<char*>(Ws) + ((size_t)kv * Rs + r) * VB;
+      const char* src = reinterpret_cast<const char*>(Wg) + ((size_t)r * Kv + kv) * VB;
+      if (VB == 16) cp_async16(dst, src, 16);
+      else cp_async8(dst, src, 8);
+    }
+    cp_async_commit();
+  }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWsComputeWarps);
+    }
+    mbar_init(redfull, kWsComputeWarps);
+    mbar_init(redempty, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+
+  const int nchunk = (Dp + KC - 1) / KC;
+  const int rot = (int)(blockIdx.x % (unsigned)nchunk);
+  const int r0 = TAPS == 2 ? 0 : 1;  // SRU never reads row 0 (x_{t-1})
+
+  if (warp == kWsComputeWarps) {
+    // ---------------- producer: TMA bulk copies of x-row chunks ----------------
+    uint32_t seq = 0;
+    for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
+      const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
+      for (int p0 = 0; p0 < l; p0 += NT) {
+        const int nt = (l - p0) < NT ? (l - p0) : NT;
+        const int64_t tp = t0 + p0;
+        for (int ch = 0; ch < nchunk; ++ch, ++seq) {
+          const int s = seq % STAGES;
+          const uint32_t ph = (seq / STAGES) & 1;
+          if (a.dbg & 1) continue;
+          mbar_wait(&empty[s], ph ^ 1);
+          const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
+          const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
+          TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
+          const bool carry_row = (r0 == 0 && tp == 0 && a.xcarry != nullptr);
+          if (!carry_row) {
+            // one 2-D TMA box [NT+1-r0 rows x XS cols] per chunk: box rows land at
+            // pitch XS (the padding columns are real neighbours, never read), rows
+            // before 0 or past L and columns past D are zero-filled by the TMA unit
+            if (lane == 0) {
+              const int nb = (kcs + BW - 1) / BW;
+              mbar_arrive_expect_tx(&full[s], (uint32_t)(nb * (NT + 1) * BXS * sizeof(TA)));
+              for (int b = 0; b < nb; ++b) tma_load_2d(xb + (size_t)b * BOXS, &tmx, d0 + b * BW, (int)(tp - 1), &full[s]);
+            }
+            continue;
+          }
+          // first pass with a carried x_{-1}: row 0 from x_carry, rows 1.. per row
+          const int nb = (kcs + BW - 1) / BW;
+          __syncwarp();
+          if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)((nt + 1) * kcs * sizeof(TA)));
+          __syncwarp();
+          for (int i = lane; i < (nt + 1) * nb; i += 32) {
+            const int r = i / nb, b = i - (i / nb) * nb;
+            const int64_t gr = tp - 1 + r;
+            const int w = (kcs - b * BW) < BW ? (kcs - b * BW) : BW;
+            const TA* src = gr >= 0 ? a.X + gr * a.ldx + d0 + b * BW : a.xcarry + d0 + b * BW;
+            bulk_g2s(xb + (size_t)b * BOXS + (size_t)r * BXS, src, (uint32_t)(w * sizeof(TA)), &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp > kWsComputeWarps) {
+    // ------------- epilogue warpgroup: sums, activations, scan, output -------------
+    const int et = tid - (kWsComputeWarps + 1) * 32;  // 0 .. kWsEpiThreads-1
+    TA c = TA(0);
+    if (et < U && a.c_in != nullptr && u0 + et < a.H) c = a.c_in[u0 + et];
+    uint32_t pass = 0;
+    for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
+      const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
+      for (int p0 = 0; p0 < l; p0 += NT, ++pass) {
+        const int nt = (l - p0) < NT ? (l - p0) : NT;
+        const int64_t tp = t0 + p0;
+        if (!(a.dbg & 2)) mbar_wait(redfull, pass & 1);
+        for (int i = et; i < ((a.dbg & 4) ? 0 : R * nt); i += kWsEpiThreads) {
+          const int r = i / nt, col = i - (i / nt) * nt;
+          TA s = TA(0);
+#pragma unroll
+          for (int w = 0; w < KG; ++w) s += red[((size_t)w * Rpad + r) * NT + col];
+          const int u = r / 3, g = r - 3 * (r / 3);
+          TA v;
+          if (CELL == SRU) v = g == 0 ? s : sigmoid_ref<TA>(s + a.bias[(size_t)(u0 + u) * 2 + g - 1]);
+          else v = g == 0 ? tanh_full(s) : sigmoid_ref<TA>(s);
+          gate[((size_t)g * U + u) * NT + col] = v;
+        }
+        epi_bar_sync();
+        if (et == 0) mbar_arrive(redempty);
+        if (et < U && !(a.dbg & 4)) {
+          TA* cand = gate + (size_t)et * NT;
+          const TA* fg = gate + (size_t)(U + et) * NT;
+          for (int col = 0; col < nt; ++col) {
+            const TA f = fg[col];
+            c = f * c + (TA(1) - f) * cand[col];
+            cand[col] = c;
+          }
+        }
+        epi_bar_sync();
+        for (int i = et; i < ((a.dbg & 4) ? 0 : U * nt); i += kWsEpiThreads) {
+          const int u = i % U, col = i / U;
+          const int unit = u0 + u;
+          if (unit < a.H) {
+            const TA cc = gate[(size_t)u * NT + col];
+            const TA o = gate[((size_t)2 * U + u) * NT + col];
+            TA h = o * tanh_full(cc);
+            if (CELL == SRU) h = h + (TA(1) - o) * a.Xhw[(tp + col) * a.ldhw + unit];
+            a.Hout[(tp + col) * a.ldh + unit] = h;
+          }
+        }
+        epi_bar_sync();
+      }
+    }
+    if (et < U && a.c_out != nullptr && u0 + et < a.H) a.c_out[u0 + et] = c;
+  } else {
+    // ---------------- consumers: FFMA over the staged chunks ----------------
+    const int tq = lane % LANES_T, kq = lane / LANES_T;
+    const int rg = warp / KG, kg = warp - (warp / KG) * KG;
+    const int kl = kg * LANES_K + kq;
+    const int rbase = rg * RH;
+    // lane-constant x offset: box of k-vector kl, row tq+1 (tap 0, column tq)
+    const int xlane = (kl >> LVPB) * BOXS + (tq + 1) * BXS + (kl & MVPB) * KV;
+    uint32_t seq = 0, pass = 0;
+    for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
+      const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
+      for (int p0 = 0; p0 < l; p0 += NT, ++pass) {
+        TA acc[RH][CT];
+#pragma unroll
+        for (int r = 0; r < RH; ++r)
+#pragma unroll
+          for (int ct = 0; ct < CT; ++ct) acc[r][ct] = TA(0);
+        for (int ch = 0; ch < nchunk; ++ch, ++seq) {
+          const int s = seq % STAGES;
+          if (!(a.dbg & 1)) mbar_wait(&full[s], (seq / STAGES) & 1);
+          const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
+          const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
+          const TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
+          // KC == KL*KV (host): every lane owns exactly one k-vector per tap per
+          // chunk, at a lane-constant offset inside the staged box
+          if (kl < kcs / KV) {
+            const TA* xl = xb + xlane;
+            const TW* wl = Ws + ((size_t)(d0 / KV + kl) * Rs + rbase) * KV;
+#pragma unroll
+            for (int tap = 0; tap < TAPS; ++tap) {
+              TA xv[CT][KV];
+#pragma unroll
+              for (int ct = 0; ct < CT; ++ct) {
+                Vec16<TA> v = lds16<TA>(xl + (size_t)(LANES_T * ct - tap) * BXS);
+#pragma unroll
+                for (int e = 0; e < KV; ++e) xv[ct][e] = round_x(v.v[e], XR);
+              }
+              const TW* wp = wl + (size_t)tap * (Dp / KV) * Rs * KV;
+#pragma unroll
+              for (int r = 0; r < RH; ++r) {
+                TA w[KV];
+                WLoad<TA, TW>::shared(wp + r * KV, w);
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+                  for (int e = 0; e < KV; ++e) acc[r][ct] = fma(w[e], xv[ct][e], acc[r][ct]);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s]);
+        }
+#pragma unroll
+        for (int r = 0; r < RH; ++r)
+#pragma unroll
+          for (int ct = 0; ct < CT; ++ct) {
+            TA v = acc[r][ct];
+#pragma unroll
+            for (int o = LANES_T; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc[r][ct] = v;
+          }
+        if (!(a.dbg & 2)) mbar_wait(redempty, (pass & 1) ^ 1);
+        if (kq == 0) {
+#pragma unroll
+          for (int r = 0; r < RH; ++r)
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct)
+              red[((size_t)kg * Rpad + rbase + r) * NT + tq + LANES_T * ct] = acc[r][ct];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(redfull);
+      }
+    }
+  }
+}
+
+}  // namespace rnnb

@@ -1,5 +1,6 @@
 // C ABI of the blocked SRU/QRNN path (see include/rnnb.h).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -104,6 +105,7 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
   a.D = (int)ly.din;
   a.Dp = ly.Dp;
   a.H = (int)ly.dh;
+  a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
   a.xround = h->mode == RNNB_BF16 ? XR_BF16 : (h->mode == RNNB_TF32 ? XR_TF32 : XR_NONE);
   return a;
 }
@@ -499,6 +501,9 @@ rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value) {
     case 3: *value = h->layers[layer].last.wsmem ? 1 : 0; return RNNB_OK;
     case 4: *value = h->layers[layer].grid; return RNNB_OK;
     case 5: *value = (int64_t)h->layers[layer].last.smem; return RNNB_OK;
+    case 6: *value = h->layers[layer].last.ws ? 1 : 0; return RNNB_OK;
+    case 7: *value = h->layers[layer].last.nt; return RNNB_OK;
+    case 8: *value = h->layers[layer].last.kc; return RNNB_OK;
     default: return fail(RNNB_EINVAL, "unknown query");
   }
 }

@@ -159,6 +159,7 @@ def test_baseline_cfg2_full(P, oracle):
         if T == 32:
             assert_f32(H[g["cfg2_T32_rows"]], g["cfg2_T32_Hrows"])
             assert_f32(c.cpu().numpy(), g["cfg2_T32_c"])
+        assert st.query(3) == 1 and st.query(6) == 1  # SMEM-resident, warp-specialised
         ref, cref, _ = oracle.run_blocked("qrnn", layers, w.X, T, return_state=True)
         assert_f32(H, ref)
         assert_f32(c.cpu().numpy(), cref[0])
