@@ -22,7 +22,7 @@
 namespace rnnb {
 
 constexpr int kWsComputeWarps = 16;
-constexpr int kWsEpiWarps = 4;
+constexpr int kWsEpiWarps = 2;
 constexpr int kWsEpiThreads = kWsEpiWarps * 32;
 constexpr int kWsThreads = (kWsComputeWarps + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group
 
@@ -51,9 +51,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
+      "r"(parity), "r"(0x100000u)  // suspend-time hint (ns): sleep instead of spinning
       : "memory");
 }
 // 2-D TMA tile load (tensor map in param space), completion on `bar`
