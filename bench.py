@@ -127,10 +127,20 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
     sec = ms_per_launch / 1e3
     mhz = pk.get("sm_max_mhz", 1965.0)
     if mode in ("f32", "f64"):
-        # FFMA pipe: 148 SMs x 128 FP32 FMA/clk x 2 FLOP (fp64: half rate on B200)
-        peak = 148 * 128 * 2 * mhz * 1e6 / 1e12 * (0.5 if mode == "f64" else 1.0)
+        # CUDA-core pipe: MEASURED_PEAKS.json has no CUDA-core figure, so use the
+        # FFMA throughput measured on this pool by tools/ffma_peak.cu
+        fp = os.path.join(REPO, "profiles", "ffma_peak.json")
+        if os.path.exists(fp):
+            with open(fp) as f:
+                peak = json.load(f)["reg3_tflops"]
+            src = "measured: tools/ffma_peak.cu register FFMA, profiles/ffma_peak.json"
+        else:
+            peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
+            src = f"nominal: 148 SMs x 128 lanes x 2 FLOP x {mhz:.0f} MHz"
+        if mode == "f64":
+            peak *= 0.5
+            src += " x 0.5 (fp64 rate)"
         pipe = "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)"
-        src = f"derived: 148 SMs x 128 lanes x 2 FLOP x sm_max_mhz {mhz:.0f} (no CUDA-core peak in MEASURED_PEAKS.json)"
     else:
         peak = pk["bf16_tflops"] * (0.5 if mode == "tf32" else 1.0)
         pipe = "tcgen05 " + mode

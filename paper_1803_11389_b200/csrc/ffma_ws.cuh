@@ -51,10 +51,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
       "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x100000u)  // suspend-time hint (ns): sleep instead of spinning
+      "r"(parity)
       : "memory");
+}
+// off-critical-path wait (producer / epilogue): back off with nanosleep so the
+// spinning warp does not steal issue slots from the FFMA consumers
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ns = 32;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+    ns = ns < 1024 ? ns * 2 : 1024;
+  }
 }
 // 2-D TMA tile load (tensor map in param space), completion on `bar`
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
@@ -199,7 +217,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
           const int s = seq % STAGES;
           const uint32_t ph = (seq / STAGES) & 1;
           if (a.dbg & 1) continue;
-          mbar_wait(&empty[s], ph ^ 1);
+          mbar_wait_sleep(&empty[s], ph ^ 1);
           const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
           const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
           TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
@@ -241,7 +259,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
       for (int p0 = 0; p0 < l; p0 += NT, ++pass) {
         const int nt = (l - p0) < NT ? (l - p0) : NT;
         const int64_t tp = t0 + p0;
-        if (!(a.dbg & 2)) mbar_wait(redfull, pass & 1);
+        mbar_wait_sleep(redfull, pass & 1);
         for (int i = et; i < ((a.dbg & 4) ? 0 : R * nt); i += kWsEpiThreads) {
           const int r = i / nt, col = i - (i / nt) * nt;
           TA s = TA(0);
@@ -341,7 +359,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             for (int o = LANES_T; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
             acc[r][ct] = v;
           }
-        if (!(a.dbg & 2)) mbar_wait(redempty, (pass & 1) ^ 1);
+        mbar_wait(redempty, (pass & 1) ^ 1);
         if (kq == 0) {
 #pragma unroll
           for (int r = 0; r < RH; ++r)
