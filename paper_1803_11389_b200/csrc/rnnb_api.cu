@@ -7,6 +7,7 @@
 
 #include "../../include/rnnb.h"
 #include "ffma_dispatch.cuh"
+#include "tc_dispatch.cuh"
 
 using namespace rnnb;
 
@@ -38,6 +39,12 @@ struct Layer {
   bool loaded = false;
   FfmaPlan last;
   int grid = 0;
+  // tensor-core path (BF16/TF32 stacks): gate-major operand weights
+  void* Wtc = nullptr;  // [3*Hpad128][tcKp] bf16 or tf32-rounded f32
+  int tcKp = 0;         // taps * Dtc, Dtc = d_in padded to the k-tile
+  int Hpad128 = 0;
+  bool last_tc = false;
+  float* bias_tc = nullptr;  // [Hpad128][2]
 };
 
 }  // namespace
@@ -48,6 +55,11 @@ struct rnnb_stack {
   void* ws[2] = {nullptr, nullptr};
   size_t ws_bytes = 0;
   int64_t last_launches = 0;
+  void* op = nullptr;     // tensor-core operand copy of a layer input, [L+1][maxD]
+  size_t op_bytes = 0;
+  float* cbuf = nullptr;  // tensor-core c chain state + flags
+  int* flags = nullptr;
+  size_t cf_bytes = 0;
   void* hostX = nullptr;  // e2e device staging
   void* hostH = nullptr;
   size_t hx_bytes = 0, hh_bytes = 0;
@@ -110,12 +122,82 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
   return a;
 }
 
+bool use_tc(const rnnb_stack* h, int64_t Tb) {
+  return (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) && Tb >= 16 && Tb <= 128 &&
+         getenv("RNNB_NO_TC") == nullptr;
+}
+
+// one layer on the tcgen05 path (tc_layer.cuh)
+rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb, float* Hout,
+                            int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
+  Layer& ly = h->layers[li];
+  const int mode = h->mode == RNNB_BF16 ? TC_BF16 : TC_TF32;
+  const int es = mode == TC_BF16 ? 2 : 4;
+  const int64_t ldop = (ly.din + 7) / 8 * 8;
+  const size_t opb = (size_t)(L + 1) * ldop * es;
+  if (h->op_bytes < opb) {
+    if (h->op) cudaFree(h->op);
+    h->op = nullptr;
+    h->op_bytes = 0;
+    CUDA_TRY(cudaMalloc(&h->op, opb));
+    h->op_bytes = opb;
+  }
+  const int nU = ly.Hpad128 / 128;
+  const size_t cfb = (size_t)ly.Hpad128 * sizeof(float) + (size_t)nU * sizeof(int);
+  if (h->cf_bytes < cfb) {
+    if (h->cbuf) cudaFree(h->cbuf);
+    h->cbuf = nullptr;
+    h->cf_bytes = 0;
+    CUDA_TRY(cudaMalloc(&h->cbuf, cfb));
+    h->cf_bytes = cfb;
+  }
+  h->flags = reinterpret_cast<int*>(h->cbuf + ly.Hpad128);
+  CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s));
+  CUDA_TRY(cudaMemsetAsync(h->cbuf, 0, cfb, s));
+  if (c_io) CUDA_TRY(cudaMemcpyAsync(h->cbuf, c_io, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  TcArgs a{};
+  a.Xhw = X;
+  a.ldhw = ldx;
+  a.Hout = Hout;
+  a.ldh = ldh;
+  a.Hop = nullptr;
+  a.bias = ly.bias_tc;
+  a.cbuf = h->cbuf;
+  a.flags = h->flags;
+  a.L = L;
+  a.T_b = (int)Tb;
+  a.H = (int)ly.dh;
+  a.Hpad = ly.Hpad128;
+  a.D = (int)ly.din;
+  const int KT = mode == TC_BF16 ? 64 : 32;
+  a.nKtap = (int)((ly.din + KT - 1) / KT);
+  a.nK = ly.tcKp / KT;
+  a.nU = nU;
+  a.nB = (int)((L + Tb - 1) / Tb);
+  int grid = 0;
+  cudaError_t e = tc_layer_run(h->kind, mode, a, ly.Wtc, ly.tcKp, h->op, ldop, h->num_sms, s, &grid);
+  if (e != cudaSuccess) return cuda_fail(e, "tc_layer launch");
+  if (c_io) CUDA_TRY(cudaMemcpyAsync(c_io, h->cbuf, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
+  ly.last_tc = true;
+  ly.grid = grid;
+  ly.last = FfmaPlan{};
+  ly.last.nt = tc_pick_n((int)Tb);
+  h->last_launches += 2;  // operand conversion + layer kernel
+  return RNNB_OK;
+}
+
 // one layer over [L x din] -> [L x dh]
 template <typename TA, typename TW>
 rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_t L, int64_t Tb,
                          TA* Hout, int64_t ldh, TA* c_io, TA* xc_io, TA* G, int64_t ldg,
                          cudaStream_t s) {
+  if constexpr (sizeof(TA) == 4) {
+    if (G == nullptr && use_tc(h, Tb))
+      return tc_layer_launch(h, li, reinterpret_cast<const float*>(X), ldx, L, Tb, reinterpret_cast<float*>(Hout),
+                             ldh, reinterpret_cast<float*>(c_io), reinterpret_cast<float*>(xc_io), s);
+  }
   Layer& ly = h->layers[li];
+  ly.last_tc = false;
   LayerArgs<TA, TW> a = make_args<TA, TW>(h, ly);
   a.X = X;
   a.ldx = ldx;
@@ -267,7 +349,11 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   for (auto& ly : h->layers) {
     if (ly.W) cudaFree(ly.W);
     if (ly.bias) cudaFree(ly.bias);
+    if (ly.Wtc) cudaFree(ly.Wtc);
+    if (ly.bias_tc) cudaFree(ly.bias_tc);
   }
+  if (h->op) cudaFree(h->op);
+  if (h->cbuf) cudaFree(h->cbuf);
   for (auto& p : h->ws)
     if (p) cudaFree(p);
   if (h->hostX) cudaFree(h->hostX);
@@ -333,6 +419,38 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
     CUDA_TRY(cudaMalloc(&ly.bias, b.size()));
     CUDA_TRY(cudaMemcpy(ly.bias, b.data(), b.size(), cudaMemcpyHostToDevice));
     ly.wbytes += b.size();
+  }
+  if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) {
+    // tensor-core layout: rows g*Hpad128 + u (gate-major), columns [tap][Dtc]
+    const int KT = h->mode == RNNB_BF16 ? 64 : 32;
+    const int64_t Dtc = (ly.din + KT - 1) / KT * KT;
+    ly.Hpad128 = (int)((ly.dh + 127) / 128 * 128);
+    ly.tcKp = (int)(T * Dtc);
+    const size_t rows_tc = (size_t)3 * ly.Hpad128;
+    std::vector<unsigned char> tc(rows_tc * ly.tcKp * ws, 0);
+    for (int g = 0; g < 3; ++g)
+      for (int64_t u = 0; u < ly.dh; ++u)
+        for (int tap = 0; tap < T; ++tap) {
+          const int m = slot(g, tap);
+          for (int64_t k = 0; k < ly.din; ++k) {
+            const float v = (float)get(m, u * ly.din + k);
+            const size_t dst = ((size_t)g * ly.Hpad128 + u) * ly.tcKp + (size_t)tap * Dtc + k;
+            if (h->mode == RNNB_BF16) reinterpret_cast<uint16_t*>(tc.data())[dst] = to_bf16(v);
+            else reinterpret_cast<float*>(tc.data())[dst] = to_tf32(v);
+          }
+        }
+    if (ly.Wtc) cudaFree(ly.Wtc), ly.Wtc = nullptr;
+    if (ly.bias_tc) cudaFree(ly.bias_tc), ly.bias_tc = nullptr;
+    CUDA_TRY(cudaMalloc(&ly.Wtc, tc.size()));
+    CUDA_TRY(cudaMemcpy(ly.Wtc, tc.data(), tc.size(), cudaMemcpyHostToDevice));
+    ly.wbytes += tc.size();
+    if (h->kind == RNNB_SRU) {
+      std::vector<float> b((size_t)ly.Hpad128 * 2, 0.f);
+      for (int64_t u = 0; u < ly.dh; ++u)
+        for (int j = 0; j < 2; ++j) b[u * 2 + j] = (float)get(3 + j, u);
+      CUDA_TRY(cudaMalloc(&ly.bias_tc, b.size() * sizeof(float)));
+      CUDA_TRY(cudaMemcpy(ly.bias_tc, b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
   }
   ly.loaded = true;
   cudaSetDevice(cur);
@@ -504,6 +622,7 @@ rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value) {
     case 6: *value = h->layers[layer].last.ws ? 1 : 0; return RNNB_OK;
     case 7: *value = h->layers[layer].last.nt; return RNNB_OK;
     case 8: *value = h->layers[layer].last.kc; return RNNB_OK;
+    case 9: *value = h->layers[layer].last_tc ? 1 : 0; return RNNB_OK;
     default: return fail(RNNB_EINVAL, "unknown query");
   }
 }

@@ -1,0 +1,19 @@
+// Host interface of the tcgen05 layer path (tc_launch.cu).
+#pragma once
+#include "ffma_dispatch.cuh"  // encode_tiled()
+#include "tc_layer.cuh"
+
+namespace rnnb {
+
+// MMA-operand copy of a layer input with a leading x_{-1} row.
+cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                          int64_t L, int D, cudaStream_t s);
+
+// One layer on the tensor-core path.  Wtc: [3*Hpad][Kp] gate-major operand
+// weights; Xop: [L+1][ldop_in] operand input (row 0 = x_{-1}).
+cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, const void* Xop, int64_t ldop_in,
+                         int num_sms, cudaStream_t s, int* grid_out);
+
+int tc_pick_n(int T_b);
+
+}  // namespace rnnb

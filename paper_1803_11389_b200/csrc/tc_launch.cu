@@ -1,0 +1,104 @@
+// Host launch of the tcgen05 layer kernel + the operand-conversion kernel.
+#include <cstdlib>
+
+#include "tc_dispatch.cuh"
+
+namespace rnnb {
+
+// X operand rows: row 0 = x_{-1} (carry or zeros), rows 1..L = x_t rounded to
+// the MMA operand type (bf16 RNE, or tf32 RNA kept in fp32 containers).
+template <int MODE>
+__global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ xcarry,
+                                  void* __restrict__ out, int64_t ldo, int64_t L, int D) {
+  const int64_t n = (L + 1) * (int64_t)D;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / D;
+    const int d = (int)(i - r * D);
+    const float v = r == 0 ? (xcarry ? xcarry[d] : 0.f) : X[(r - 1) * ldx + d];
+    if (MODE == TC_BF16)
+      reinterpret_cast<__nv_bfloat16*>(out)[r * ldo + d] = __float2bfloat16_rn(v);
+    else
+      reinterpret_cast<float*>(out)[r * ldo + d] = round_x(v, XR_TF32);
+  }
+}
+
+cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                          int64_t L, int D, cudaStream_t s) {
+  const int64_t n = (L + 1) * (int64_t)D;
+  const int bs = 256;
+  const int grid = (int)((n + bs - 1) / bs < 148 * 16 ? (n + bs - 1) / bs : 148 * 16);
+  if (mode == TC_BF16) to_operand_kernel<TC_BF16><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
+  else to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
+  return cudaGetLastError();
+}
+
+static bool make_map(CUtensorMap* tm, CUtensorMapDataType dt, int es, const void* base, uint64_t inner,
+                     uint64_t outer, uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
+  EncodeTiledFn enc = encode_tiled();
+  if (!enc) return false;
+  cuuint64_t gdim[2] = {inner, outer};
+  cuuint64_t gstride[1] = {ld_elems * (uint64_t)es};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(tm, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int CELL, int MODE, int N>
+static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx, int grid,
+                             cudaStream_t s) {
+  using C = TcCfg<MODE, N>;
+  auto k = tc_layer_kernel<CELL, MODE, N>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k<<<grid, kTcThreads, C::SMEM, s>>>(a, tw, tx);
+  return cudaGetLastError();
+}
+
+int tc_pick_n(int T_b) {
+  if (T_b <= 16) return 16;
+  if (T_b <= 32) return 32;
+  if (T_b <= 64) return 64;
+  return 128;
+}
+
+template <int CELL, int MODE>
+static cudaError_t run_n(int N, const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx, int grid,
+                         cudaStream_t s) {
+  switch (N) {
+    case 16: return launch_tc<CELL, MODE, 16>(a, tw, tx, grid, s);
+    case 32: return launch_tc<CELL, MODE, 32>(a, tw, tx, grid, s);
+    case 64: return launch_tc<CELL, MODE, 64>(a, tw, tx, grid, s);
+    default: return launch_tc<CELL, MODE, 128>(a, tw, tx, grid, s);
+  }
+}
+
+cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, const void* Xop, int64_t ldop_in,
+                         int num_sms, cudaStream_t s, int* grid_out) {
+  const int N = tc_pick_n(a.T_b);
+  const int es = mode == TC_BF16 ? 2 : 4;
+  const int KT = mode == TC_BF16 ? 64 : 32;
+  const CUtensorMapDataType dt = mode == TC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+  CUtensorMap tw, tx;
+  if (!make_map(&tw, dt, es, Wtc, (uint64_t)Kp, (uint64_t)3 * a.Hpad, (uint64_t)Kp, KT, 128))
+    return cudaErrorInvalidValue;
+  // operand X has L+1 rows (row 0 = x_{-1}); the kernel addresses row t+1
+  if (!make_map(&tx, dt, es, Xop, (uint64_t)a.D, (uint64_t)(a.L + 1), (uint64_t)ldop_in, KT, N))
+    return cudaErrorInvalidValue;
+  const int nitems = a.nU * a.nB;
+  const int grid = nitems < num_sms ? nitems : num_sms;
+  if (grid_out) *grid_out = grid;
+  if (cell == SRU) {
+    if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tw, tx, grid, s);
+    return run_n<SRU, TC_TF32>(N, a, tw, tx, grid, s);
+  }
+  if (mode == TC_BF16) return run_n<QRNN, TC_BF16>(N, a, tw, tx, grid, s);
+  return run_n<QRNN, TC_TF32>(N, a, tw, tx, grid, s);
+}
+
+}  // namespace rnnb

@@ -1,0 +1,323 @@
+// Tensor-core (tcgen05 + TMEM + TMA) blocked SRU/QRNN layer kernel, sm_100a.
+//
+// Reference path: rnnblock run_blocked (blocked.py:221-268) with the block
+// projection precompute_gates_* (blocked.py:123-150), the c-sweep
+// (blocked.py:153-176) and finalize_outputs (blocked.py:179-193) fused.
+//
+// Work item = (unit tile u of 128 hidden units, time block b of T_b steps).
+// For one item the CTA computes, per gate g in {cand, forget, out/highway},
+//     P_g[128 x N] = W_g[u-tile, :] . X_block^T          (N = T_b padded to 16)
+// with K = taps*D: the QRNN x_{t-1} tap multiplies the SAME x tile fetched one
+// row earlier (row -1 is zero-filled by TMA), exactly Xprev of blocked.py:143.
+// The three accumulators live in TMEM (3*N columns, double-buffered when
+// they fit) and never touch HBM; the epilogue warps read them with
+// tcgen05.ld (thread = TMEM lane = hidden unit), apply bias/activations, run
+// the sequential c-scan over the block and write h.
+//
+// Items are processed time-block-major by a persistent grid, so different
+// time blocks' projections run concurrently on different SMs (the weights of
+// a layer stay L2-resident and are re-read once per block, the reference's
+// "one weight fetch per block" model); only the cheap scan is chained: the
+// epilogue of (u, b) waits for the c state published by (u, b-1) through a
+// per-tile flag (acquire/release at gpu scope).  Items are claimed in
+// increasing order and every dependency points to a smaller item, so with
+// all CTAs co-resident the chain cannot deadlock.
+//
+// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
+// issuer (one elected lane), warps 2..5 epilogue (TMEM lane quadrant w%4).
+#pragma once
+#include <cuda.h>
+
+#include "common.cuh"
+#include "ffma_ws.cuh"  // mbarrier / TMA helpers
+
+namespace rnnb {
+
+enum TcMode : int { TC_BF16 = 0, TC_TF32 = 1 };
+
+struct TcArgs {
+  const float* Xhw;   // SRU highway source x (fp32, raw), row stride ldhw
+  int64_t ldhw;
+  float* Hout;        // fp32 h [L][ldh]
+  int64_t ldh;
+  void* Hop;          // optional MMA-operand copy of h for the next layer (bf16 or tf32-rounded f32), [L][ldop]
+  int64_t ldop;
+  const float* bias;  // SRU [Hpad][2] (b_forget, b_highway) or nullptr
+  float* cbuf;        // [Hpad] carried c state (in: c_0, out: c_T)
+  int* flags;         // [nU] number of time blocks whose scan is published
+  int64_t L;
+  int T_b;
+  int H, Hpad, D;
+  int nK;             // k-tiles per row (taps * Dp / KT)
+  int nKtap;          // k-tiles per tap
+  int nU, nB;
+};
+
+template <int MODE> struct TcT;
+template <> struct TcT<TC_BF16> {
+  static constexpr int ES = 2;   // operand element bytes
+  static constexpr int KT = 64;  // k-tile: 128 bytes = one SW128 row
+  static constexpr int UK = 16;  // K per tcgen05.mma (kind::f16)
+  static constexpr uint32_t FMT = 1;  // BF16
+};
+template <> struct TcT<TC_TF32> {
+  static constexpr int ES = 4;
+  static constexpr int KT = 32;
+  static constexpr int UK = 8;   // K per tcgen05.mma (kind::tf32)
+  static constexpr uint32_t FMT = 2;  // TF32
+};
+
+constexpr int kTcThreads = 192;
+
+// ---- tcgen05 wrappers (PTX ISA 8.7, sm_100a) ----
+__device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(dst_smem)),
+               "r"(ncols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+}
+__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(taddr), "r"(ncols));
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+// D[tmem] (+)= A[smem desc] . B[smem desc]^T, kind selected by MODE
+template <int MODE>
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  if (MODE == TC_BF16)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc));
+}
+// arrive on an mbarrier once all previously issued tcgen05.mma have completed
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// K-major, 128-byte-swizzled operand tile (rows of 128 B, 8-row atoms 1 KB apart)
+__device__ __forceinline__ uint64_t sw128_desc(const void* smem_tile) {
+  const uint64_t addr = smem_u32(smem_tile);
+  uint64_t d = 0;
+  d |= (addr >> 4) & 0x3FFFull;        // start address
+  d |= (uint64_t)1 << 16;              // leading byte offset (ignored for SW128 K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;    // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;              // layout: SWIZZLE_128B
+  return d;
+}
+
+template <int MODE>
+__host__ __device__ constexpr uint32_t tc_idesc(int M, int N) {
+  return (1u << 4)                      // D format F32
+         | (TcT<MODE>::FMT << 7)        // A format
+         | (TcT<MODE>::FMT << 10)       // B format
+         | ((uint32_t)(N >> 3) << 17)   // N / 8
+         | ((uint32_t)(M >> 4) << 24);  // M / 16
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ float ld_cg(const float* p) {
+  float v;
+  asm volatile("ld.global.cg.f32 %0, [%1];\n" : "=f"(v) : "l"(p) : "memory");
+  return v;
+}
+// named barrier 2 over the four epilogue warps
+__device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
+
+template <int MODE, int N>
+struct TcCfg {
+  static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
+  static constexpr int A_BYTES = 128 * 128;  // one gate tile: 128 rows x 128 B
+  static constexpr int B_BYTES = N * 128;
+  static constexpr int STAGE_BYTES = 3 * A_BYTES + B_BYTES;
+  static constexpr int STAGES = (4 * STAGE_BYTES + 2048 <= 227 * 1024) ? 4 : 3;
+  static constexpr int ACC_COLS = 3 * N;
+  static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;
+  static constexpr int TMEM_COLS = (NACC * ACC_COLS <= 32) ? 32 : (NACC * ACC_COLS <= 64) ? 64
+                                   : (NACC * ACC_COLS <= 128) ? 128 : (NACC * ACC_COLS <= 256) ? 256 : 512;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int CELL, int MODE, int N>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_layer_kernel(TcArgs a, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX) {
+  using C = TcCfg<MODE, N>;
+  extern __shared__ __align__(1024) unsigned char tsm_raw[];
+  unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + (size_t)C::STAGES * C::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* acc_full = empty + C::STAGES;
+  uint64_t* acc_empty = acc_full + 2;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nitems = a.nU * a.nB;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc(tmem_base_smem, C::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_base_smem;
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
+        const int t0 = b * a.T_b;
+        for (int kt = 0; kt < a.nK; ++kt, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait_sleep(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
+          for (int g = 0; g < 3; ++g)
+            tma_load_2d(st + g * C::A_BYTES, &tmW, kt * C::KT, g * a.Hpad + u * 128, &full[s]);
+          const int tap = kt >= a.nKtap ? 1 : 0;
+          const int kx = (kt - tap * a.nKtap) * C::KT;
+          // operand row r holds x_{r-1}: block rows t0.. for tap 0, t0-1.. for tap 1
+          tma_load_2d(st + 3 * C::A_BYTES, &tmX, kx, t0 + 1 - tap, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (one lane) ----------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc_idesc<MODE>(128, N);
+      uint32_t it = 0, acc_it = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
+        const int ab = acc_it % C::NACC;
+        mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dbase = tmem + ab * C::ACC_COLS;
+        for (int kt = 0; kt < a.nK; ++kt, ++it) {
+          const int s = it % C::STAGES;
+          mbar_wait(&full[s], (it / C::STAGES) & 1);
+          tc_fence_after();
+          unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
+          const uint64_t bdesc0 = sw128_desc(st + 3 * C::A_BYTES);
+#pragma unroll
+          for (int g = 0; g < 3; ++g) {
+            const uint64_t adesc0 = sw128_desc(st + g * C::A_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < C::KT / C::UK; ++kk) {
+              // advance the start address along K inside the 128-B swizzle row
+              const uint64_t koff = (uint64_t)((kk * C::UK * C::ES) >> 4);
+              tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kt | kk) != 0);
+            }
+          }
+          tc_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+        }
+        tc_commit(&acc_full[ab]);  // accumulators of this item complete
+      }
+    }
+  } else {
+    // ---------------- epilogue: 4 warps, thread = TMEM lane = unit ----------------
+    const int q = warp & 3;                 // TMEM lane quadrant this warp may access
+    const int row = q * 32 + lane;          // unit within the tile
+    uint32_t acc_it = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
+      const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
+      const int64_t t0 = (int64_t)b * a.T_b;
+      const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
+      const int unit = u * 128 + row;
+      const int ab = acc_it % C::NACC;
+      mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
+      tc_fence_after();
+      float bf = 0.f, br = 0.f;
+      if (CELL == SRU && a.bias) {
+        bf = a.bias[(size_t)unit * 2];
+        br = a.bias[(size_t)unit * 2 + 1];
+      }
+      // wait for the c state of this unit tile after block b-1
+      if (threadIdx.x == 64) {
+        while (ld_acquire(&a.flags[u]) < b) __nanosleep(64);
+      }
+      tc_epi_sync();
+      float c = ld_cg(&a.cbuf[unit]);
+      const uint32_t tb = tmem + ab * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+      for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
+        float pz[16], pf[16], po[16];
+        tmem_ld16(tb + 0 * N + c0, pz);
+        tmem_ld16(tb + 1 * N + c0, pf);
+        tmem_ld16(tb + 2 * N + c0, po);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int col = c0 + j;
+          if (col < l && unit < a.H) {
+            float z, f, o;
+            if (CELL == SRU) {
+              z = pz[j];
+              f = sigmoid_ref<float>(pf[j] + bf);
+              o = sigmoid_ref<float>(po[j] + br);
+            } else {
+              z = tanh_full(pz[j]);
+              f = sigmoid_ref<float>(pf[j]);
+              o = sigmoid_ref<float>(po[j]);
+            }
+            c = f * c + (1.f - f) * z;
+            float h = o * tanh_full(c);
+            if (CELL == SRU) h = h + (1.f - o) * a.Xhw[(t0 + col) * a.ldhw + unit];
+            a.Hout[(t0 + col) * a.ldh + unit] = h;
+            if (a.Hop) {
+              if (MODE == TC_BF16)
+                reinterpret_cast<__nv_bfloat16*>(a.Hop)[(t0 + col) * a.ldop + unit] = __float2bfloat16_rn(h);
+              else
+                reinterpret_cast<float*>(a.Hop)[(t0 + col) * a.ldop + unit] = round_x(h, XR_TF32);
+            }
+          }
+        }
+      }
+      // TMEM buffer can be refilled
+      tc_fence_before();
+      mbar_arrive(&acc_empty[ab]);
+      if (unit < a.Hpad) a.cbuf[unit] = c;
+      __threadfence();
+      tc_epi_sync();
+      if (threadIdx.x == 64) st_release(&a.flags[u], b + 1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+}  // namespace rnnb

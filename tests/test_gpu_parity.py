@@ -342,3 +342,55 @@ def _sru_highway_fix(oracle, rl, xr, x, T):
     # H = r tanh c + (1-r) xr  ->  replace xr by x: add (1-r)(x - xr)
     r = 0.5 * (1.0 + _np.tanh(0.5 * (xr.astype(_np.float64) @ rl[2].T.astype(_np.float64) + rl[4])))
     return (H + (1.0 - r) * (x.astype(_np.float64) - xr.astype(_np.float64))).astype(_np.float32)
+
+
+# ---------------------------------------------------------------------------
+# tcgen05 tensor-core path (T_b in [16, 128] for bf16 / tf32 stacks)
+
+
+@pytest.mark.parametrize("kind", ["sru", "qrnn"])
+@pytest.mark.parametrize("mode", ["bf16", "tf32"])
+def test_tensor_core_path_matches_oracle_on_rounded_operands(P, oracle, kind, mode, monkeypatch):
+    """TC kernel vs the oracle run on operands rounded like the MMA sees them
+    (per-layer bound 1e-5 tf32 / 1e-3 bf16), odd sizes: H=300 (3 unit tiles,
+    padded), D=200 (partial k-tile), L=777 (remainder block)."""
+    import torch
+    d = 200 if kind == "qrnn" else 300
+    h = 300
+    layers = oracle.generate_layers(kind, d, h, 1, 41, np.float32)
+    X = np.random.default_rng(9).standard_normal((777, d)).astype(np.float32)
+    st = P.DeviceStack(kind, layers, mode=mode)
+    rnd = _round_tf32 if mode == "tf32" else _round_bf16
+    rl = [rnd(m) if m.ndim == 2 else m for m in layers[0]]
+    for T in (16, 32, 48, 64, 100, 128):
+        Ht = st.forward(torch.from_numpy(X).cuda(), T)
+        assert st.query(9) == 1, "tensor-core kernel did not run"
+        H = Ht.cpu().numpy()
+        if kind == "sru":
+            ref = _sru_highway_fix(oracle, rl, rnd(X), X, T)
+        else:
+            ref = oracle.run_blocked(kind, [rl], rnd(X), T)
+        assert normwise(H, ref) <= (1e-5 if mode == "tf32" else 1e-3), (T, normwise(H, ref))
+        monkeypatch.setenv("RNNB_NO_TC", "1")
+        Hf = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
+        monkeypatch.delenv("RNNB_NO_TC")
+        assert st.query(9) == 0
+        assert normwise(H, Hf) <= (1e-5 if mode == "tf32" else 1e-3)
+    st.close()
+
+
+def test_tensor_core_streaming_carry(P, oracle):
+    """c and x_carry across calls on the TC path (operand row 0 = x_carry)."""
+    import torch
+    layers = oracle.generate_layers("qrnn", 256, 256, 2, 43, np.float32)
+    X = np.random.default_rng(10).standard_normal((512, 256)).astype(np.float32)
+    st = P.DeviceStack("qrnn", layers, mode="bf16")
+    Xd = torch.from_numpy(X).cuda()
+    whole = st.forward(Xd, 32).cpu().numpy()
+    c = torch.zeros(512, device="cuda")
+    xc = torch.zeros(512, device="cuda")
+    a = st.forward(Xd[:256].contiguous(), 32, c_state=c, x_carry=xc).cpu().numpy()
+    b = st.forward(Xd[256:].contiguous(), 32, c_state=c, x_carry=xc).cpu().numpy()
+    assert st.query(9) == 1
+    assert normwise(np.concatenate([a, b]), whole) <= 1e-6
+    st.close()
