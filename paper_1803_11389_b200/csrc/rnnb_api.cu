@@ -143,7 +143,10 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
     h->op_bytes = opb;
   }
   const int nU = ly.Hpad128 / 128;
-  const size_t cfb = (size_t)ly.Hpad128 * sizeof(float) + (size_t)nU * sizeof(int);
+  const int64_t nB = (L + Tb - 1) / Tb;
+  // cbuf [Hpad] | aggA, aggB, incl [nB][Hpad] | status [nB][nU]
+  const size_t plane = (size_t)nB * ly.Hpad128;
+  const size_t cfb = ((size_t)ly.Hpad128 + 3 * plane) * sizeof(float) + (size_t)nB * nU * sizeof(int);
   if (h->cf_bytes < cfb) {
     if (h->cbuf) cudaFree(h->cbuf);
     h->cbuf = nullptr;
@@ -151,9 +154,11 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
     CUDA_TRY(cudaMalloc(&h->cbuf, cfb));
     h->cf_bytes = cfb;
   }
-  h->flags = reinterpret_cast<int*>(h->cbuf + ly.Hpad128);
+  float* aggA = h->cbuf + ly.Hpad128;
+  int* status = reinterpret_cast<int*>(aggA + 3 * plane);
   CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s));
-  CUDA_TRY(cudaMemsetAsync(h->cbuf, 0, cfb, s));
+  CUDA_TRY(cudaMemsetAsync(h->cbuf, 0, ly.Hpad128 * sizeof(float), s));
+  CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)nB * nU * sizeof(int), s));
   if (c_io) CUDA_TRY(cudaMemcpyAsync(h->cbuf, c_io, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
   TcArgs a{};
   a.Xhw = X;
@@ -163,7 +168,10 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.Hop = nullptr;
   a.bias = ly.bias_tc;
   a.cbuf = h->cbuf;
-  a.flags = h->flags;
+  a.aggA = aggA;
+  a.aggB = aggA + plane;
+  a.incl = aggA + 2 * plane;
+  a.status = status;
   a.L = L;
   a.T_b = (int)Tb;
   a.H = (int)ly.dh;
@@ -173,7 +181,8 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.nKtap = (int)((ly.din + KT - 1) / KT);
   a.nK = ly.tcKp / KT;
   a.nU = nU;
-  a.nB = (int)((L + Tb - 1) / Tb);
+  a.nB = (int)nB;
+  a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
   int grid = 0;
   cudaError_t e = tc_layer_run(h->kind, mode, a, ly.Wtc, ly.tcKp, h->op, ldop, h->num_sms, s, &grid);
   if (e != cudaSuccess) return cuda_fail(e, "tc_layer launch");

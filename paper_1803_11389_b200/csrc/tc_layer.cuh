@@ -44,13 +44,17 @@ struct TcArgs {
   int64_t ldop;
   const float* bias;  // SRU [Hpad][2] (b_forget, b_highway) or nullptr
   float* cbuf;        // [Hpad] carried c state (in: c_0, out: c_T)
-  int* flags;         // [nU] number of time blocks whose scan is published
+  int* status;        // [nB][nU] look-back status: 0 none, 1 aggregate, 2 inclusive
+  float* aggA;        // [nB][Hpad] block carry map c_out = A c_in + B
+  float* aggB;
+  float* incl;        // [nB][Hpad] c after the block (inclusive prefix)
   int64_t L;
   int T_b;
   int H, Hpad, D;
   int nK;             // k-tiles per row (taps * Dp / KT)
   int nKtap;          // k-tiles per tap
   int nU, nB;
+  int dbg;            // RNNB_DEBUG bits (timing experiments): 16 = skip the c-chain wait
 };
 
 template <int MODE> struct TcT;
@@ -100,6 +104,17 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 // 32 lanes x 32 bit, 16 consecutive columns -> 16 registers per thread
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
@@ -250,8 +265,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ---------------- epilogue: 4 warps, thread = TMEM lane = unit ----------------
+    // Per item: (A) activations for every step of the block, written back over
+    // the accumulators with tcgen05.st, and the block's affine carry map
+    // c_out = Ablk * c_in + Bblk (independent of earlier blocks) published as
+    // an AGGREGATE; (B) decoupled look-back over earlier blocks' aggregates /
+    // INCLUSIVE carries of the same unit tile to get c_in, then publish this
+    // block's INCLUSIVE carry; (C) the sequential c-recurrence of the block from
+    // c_in (blocked.py:153-162) and the output mix, h stores.
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;          // unit within the tile
+    const int et = threadIdx.x - 64;        // 0..127
+    __shared__ int s_status;
     uint32_t acc_it = 0;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
       const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
@@ -266,13 +290,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         bf = a.bias[(size_t)unit * 2];
         br = a.bias[(size_t)unit * 2 + 1];
       }
-      // wait for the c state of this unit tile after block b-1
-      if (threadIdx.x == 64) {
-        while (ld_acquire(&a.flags[u]) < b) __nanosleep(64);
-      }
-      tc_epi_sync();
-      float c = ld_cg(&a.cbuf[unit]);
       const uint32_t tb = tmem + ab * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+      // (A) activations + block aggregate
+      float Ablk = 1.f, Bblk = 0.f;
       for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
         float pz[16], pf[16], po[16];
         tmem_ld16(tb + 0 * N + c0, pz);
@@ -280,21 +300,77 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tmem_ld16(tb + 2 * N + c0, po);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
+          if (CELL == SRU) {
+            pf[j] = sigmoid_ref<float>(pf[j] + bf);
+            po[j] = sigmoid_ref<float>(po[j] + br);
+          } else {
+            pz[j] = tanh_full(pz[j]);
+            pf[j] = sigmoid_ref<float>(pf[j]);
+            po[j] = sigmoid_ref<float>(po[j]);
+          }
+          if (c0 + j < l) {
+            Bblk = pf[j] * Bblk + (1.f - pf[j]) * pz[j];
+            Ablk = pf[j] * Ablk;
+          }
+        }
+        tmem_st16(tb + 0 * N + c0, pz);
+        tmem_st16(tb + 1 * N + c0, pf);
+        tmem_st16(tb + 2 * N + c0, po);
+      }
+      tmem_st_wait();
+      const size_t sidx = (size_t)b * a.Hpad + unit;
+      a.aggA[sidx] = Ablk;
+      a.aggB[sidx] = Bblk;
+      __threadfence();
+      tc_epi_sync();
+      if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 1);
+      // (B) look back
+      float cin;
+      {
+        float Aacc = 1.f, Bacc = 0.f;  // map from c after block j to c after block b-1
+        int j = b - 1;
+        while (true) {
+          if (j < 0) {
+            cin = Aacc * ld_cg(&a.cbuf[unit]) + Bacc;
+            break;
+          }
+          if (et == 0) {
+            int st;
+            while ((st = ld_acquire(&a.status[(size_t)j * a.nU + u])) == 0) __nanosleep(32);
+            s_status = st;
+          }
+          tc_epi_sync();
+          const int st = s_status;
+          tc_epi_sync();
+          const size_t jidx = (size_t)j * a.Hpad + unit;
+          if (st == 2) {
+            cin = Aacc * ld_cg(&a.incl[jidx]) + Bacc;
+            break;
+          }
+          const float Aj = ld_cg(&a.aggA[jidx]), Bj = ld_cg(&a.aggB[jidx]);
+          Bacc = Aacc * Bj + Bacc;
+          Aacc = Aacc * Aj;
+          --j;
+        }
+      }
+      a.incl[sidx] = Ablk * cin + Bblk;
+      __threadfence();
+      tc_epi_sync();
+      if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 2);
+      // (C) sequential recurrence from c_in and the output mix
+      float c = cin;
+      for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
+        float z[16], f[16], o[16];
+        tmem_ld16(tb + 0 * N + c0, z);
+        tmem_ld16(tb + 1 * N + c0, f);
+        tmem_ld16(tb + 2 * N + c0, o);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
           const int col = c0 + j;
           if (col < l && unit < a.H) {
-            float z, f, o;
-            if (CELL == SRU) {
-              z = pz[j];
-              f = sigmoid_ref<float>(pf[j] + bf);
-              o = sigmoid_ref<float>(po[j] + br);
-            } else {
-              z = tanh_full(pz[j]);
-              f = sigmoid_ref<float>(pf[j]);
-              o = sigmoid_ref<float>(po[j]);
-            }
-            c = f * c + (1.f - f) * z;
-            float h = o * tanh_full(c);
-            if (CELL == SRU) h = h + (1.f - o) * a.Xhw[(t0 + col) * a.ldhw + unit];
+            c = f[j] * c + (1.f - f[j]) * z[j];
+            float h = o[j] * tanh_full(c);
+            if (CELL == SRU) h = h + (1.f - o[j]) * a.Xhw[(t0 + col) * a.ldhw + unit];
             a.Hout[(t0 + col) * a.ldh + unit] = h;
             if (a.Hop) {
               if (MODE == TC_BF16)
@@ -308,10 +384,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // TMEM buffer can be refilled
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
-      if (unit < a.Hpad) a.cbuf[unit] = c;
-      __threadfence();
-      tc_epi_sync();
-      if (threadIdx.x == 64) st_release(&a.flags[u], b + 1);
+      if (b == a.nB - 1 && unit < a.Hpad) a.cbuf[unit] = c;  // c_T of the sequence
     }
   }
   tc_fence_before();
