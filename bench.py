@@ -61,53 +61,53 @@ def peaks():
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled every ~2 ms during the timed
+    region through NVML (nvidia_ml_py), nvidia-smi as a fallback."""
+
+    # NVML clocks-event-reason bits (nvml.h)
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.sm, self.mx, self.reasons = [], None, set()
+        self._stop = threading.Event()
+        self.thread = None
+        self.nvml = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-            time.sleep(0.15)
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 8:
-                self.rows.append(parts)
+            def loop():
+                while not self._stop.is_set():
+                    try:
+                        self.sm.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                        bits = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        for k, n in self.REASONS.items():
+                            if bits & k:
+                                self.reasons.add(n)
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+            self.thread = threading.Thread(target=loop, daemon=True)
+            self.thread.start()
+            time.sleep(0.01)
+        except Exception:
+            self.nvml = None
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.1)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        reasons = set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in self.rows:
-            for n, v in zip(names, r[4:8]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"], "samples": 0}
+        time.sleep(0.004)
+        self._stop.set()
+        self.thread.join(timeout=1)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml, 2 ms"}
 
 
 # ---------------------------------------------------------------------------
@@ -171,6 +171,58 @@ def load_traffic(workload, T_b, mode):
     return d.get(f"{workload}/{mode}/T{T_b}")
 
 
+def time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_for=None):
+    """Per T_b: W warm-up forwards, then K forwards each bracketed by CUDA
+    events on the launching stream with an L2 flush in between (outside the
+    events); max over ranks."""
+    import torch
+    stream = torch.cuda.current_stream()
+    dev = X.device
+    dist = world > 1
+    results = {}
+    for T_b in blocks:
+        for _ in range(args.warmup):
+            st.forward(X, T_b, out=out)
+        torch.cuda.synchronize()
+        launches = st.last_launches
+        tc = [bool(st.query(9, li)) for li in range(st.n_layers)]
+        ws = [bool(st.query(6, li)) for li in range(st.n_layers)]
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if dist:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        sampler = None
+        if clocks_for == T_b and rank == 0:
+            sampler = ClockSampler(local_rank)
+            sampler.start()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # L2 flush, outside the events
+            ev[i][0].record(stream)
+            st.forward(X, T_b, out=out)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            torch.distributed.barrier()
+        clocks = sampler.stop() if sampler is not None else None
+        ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+        ms_step = sum(ms) / len(ms)
+        if dist:
+            t = torch.tensor([ms_step], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms_step = float(t.item())
+        results[T_b] = {"ms_per_step": ms_step, "ms_min": min(ms), "launches": launches, "clocks": clocks,
+                        "tcgen05": tc, "ffma_ws": ws}
+    return results
+
+
+def kernel_name(r):
+    if all(r["tcgen05"]):
+        return "tc_layer (tcgen05 + TMEM + TMA, look-back carry)"
+    if all(r["ffma_ws"]):
+        return "ffma_ws (TMA producer + mbarrier ring + epilogue warps)"
+    return "ffma_layer"
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1803_11389_b200 as P
@@ -185,50 +237,24 @@ def run_ours(args, rank, world, local_rank):
     X = torch.from_numpy(w.X.astype(st.np_dtype)).to(dev)
     L = w.seq_len
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-    stream = torch.cuda.current_stream()
     blocks = list(w.block_sizes) if args.sweep else []
     if args.block not in blocks:
         blocks.append(args.block)
     blocks = sorted(set(blocks))
     out = torch.empty((L, st.d_h[-1]), dtype=dt, device=dev)
+    results = time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_for=args.block)
 
-    def one(T_b):
-        st.forward(X, T_b, out=out)
-
-    dist = world > 1
-    results = {}
-    sampler = None
-    for T_b in blocks:
-        headline = T_b == args.block
-        for _ in range(args.warmup):
-            one(T_b)
-        torch.cuda.synchronize()
-        launches = st.last_launches
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        if dist:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-        if headline and rank == 0:
-            sampler = ClockSampler(local_rank)
-            sampler.start()
-        for i in range(args.steps):
-            flush.fill_(float(i))  # L2 flush, outside the events
-            ev[i][0].record(stream)
-            one(T_b)
-            ev[i][1].record(stream)
-        torch.cuda.synchronize()
-        if dist:
-            torch.distributed.barrier()
-        clocks = sampler.stop() if (headline and sampler is not None) else None
-        ms = [a.elapsed_time(b) for a, b in ev]
-        ms_step = sum(ms) / len(ms)
-        if dist:
-            t = torch.tensor([ms_step], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ms_step = float(t.item())
-        results[T_b] = {"ms_per_step": ms_step, "ms_min": min(ms), "launches": launches, "clocks": clocks}
+    # the same workload in the tensor-core numerics modes (reported beside, not the headline)
+    extra = {}
+    for m in [m for m in args.extra_modes.split(",") if m and m != args.mode]:
+        sm = P.DeviceStack(w.kind, w.layers, mode=m, device=local_rank)
+        outm = torch.empty((L, sm.d_h[-1]), dtype=sm.dtype, device=dev)
+        Xm = X if sm.dtype == dt else X.to(sm.dtype)
+        extra[m] = time_sweep(sm, Xm, outm, blocks, args, rank, world, local_rank, flush)
+        sm.close()
 
     # end-to-end through the public C-ABI host entry point (pinned host buffers)
+    dist = world > 1
     Xh = torch.from_numpy(w.X.astype(st.np_dtype)).pin_memory()
     Hh = torch.empty((L, st.d_h[-1]), dtype=dt).pin_memory()
     Xn, Hn = Xh.numpy(), Hh.numpy()
@@ -256,13 +282,18 @@ def run_ours(args, rank, world, local_rank):
         st.close()
         return None
     pk, pk_src = peaks()
-    sweep = {}
-    for T_b, r in results.items():
-        rf = roofline_for(w, T_b, args.mode, r["ms_per_step"] / (r["launches"] or 1), r["launches"] or 1,
-                          pk, load_traffic(args.workload, T_b, args.mode))
-        sweep[str(T_b)] = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
-                           "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"],
-                           "tflops": rf["achieved"], "hbm_model_frac": rf["hbm_model"]["frac"]}
+
+    def sweep_of(res, mode):
+        out_ = {}
+        for T_b, r in res.items():
+            rf = roofline_for(w, T_b, mode, r["ms_per_step"] / (r["launches"] or 1), r["launches"] or 1,
+                              pk, None)
+            out_[str(T_b)] = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
+                              "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"],
+                              "tflops": rf["achieved"], "pipe": rf["pipe"], "kernel": kernel_name(r),
+                              "hbm_model_frac": rf["hbm_model"]["frac"]}
+        return out_
+
     head = results[args.block]
     roof = roofline_for(w, args.block, args.mode, head["ms_per_step"] / (head["launches"] or 1),
                         head["launches"] or 1, pk, load_traffic(args.workload, args.block, args.mode))
@@ -272,7 +303,7 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": round(L * world / (head["ms_per_step"] / 1e3), 1), "unit": UNIT,
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(head["ms_per_step"], 5), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": {"f32": "f32", "f64": "f64", "bf16": "bf16", "tf32": "tf32"}[args.mode],
+        "scaling": "weak", "vs_baseline": None, "dtype": args.mode,
         "data": "synthetic (seeded PCG64, BASELINE.json distributions)",
         "config": {"workload": args.workload, "cell": w.kind.value, "d_in": int(w.X.shape[1]),
                    "d_h": int(w.layers[-1].d_h), "n_layers": len(w.layers), "seq_len": L,
@@ -282,12 +313,12 @@ def run_ours(args, rank, world, local_rank):
                    "weights_smem_resident": resident,
                    "units_per_cta": [st.query(2, li) for li in range(st.n_layers)],
                    "grid": [st.query(4, li) for li in range(st.n_layers)],
-                   "kernel": ["ffma_ws (TMA producer + mbarrier ring + epilogue warp)" if st.query(6, li)
-                              else "ffma_layer" for li in range(st.n_layers)]},
+                   "kernel": kernel_name(head)},
         "e2e": e2e,
         "gpu_launches": int(head["launches"] * args.steps),
         "roofline": roof,
-        "sweep": sweep,
+        "sweep": sweep_of(results, args.mode),
+        "modes": {m: sweep_of(r, m) for m, r in extra.items()},
         "clocks": head["clocks"],
     }
     if args.cpu_baseline:
@@ -369,6 +400,8 @@ def main():
     ap.add_argument("--block", type=int, default=32)
     ap.add_argument("--mode", default="f32", choices=("f32", "f64", "bf16", "tf32"))
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
+    ap.add_argument("--extra-modes", default="bf16,tf32",
+                    help="tensor-core numerics modes timed beside the headline mode")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-sample", type=int, default=512, help="time steps in the CPU sample")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
