@@ -168,7 +168,8 @@ def load_traffic(workload, T_b, mode):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get(f"{workload}/{mode}/T{T_b}")
+    e = d.get(f"{workload}/{mode}/T{T_b}")
+    return None if e is None else e["dram_bytes_per_launch"]
 
 
 def time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_for=None):
