@@ -72,6 +72,7 @@ template <> struct TcT<TC_TF32> {
 };
 
 constexpr int kTcThreads = 192;
+constexpr int kLB = 32;  // look-back depth (aggregates composed per block)
 
 // ---- tcgen05 wrappers (PTX ISA 8.7, sm_100a) ----
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
@@ -275,7 +276,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;          // unit within the tile
     const int et = threadIdx.x - 64;        // 0..127
-    __shared__ int s_status;
     uint32_t acc_it = 0;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
       const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
@@ -324,34 +324,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __threadfence();
       tc_epi_sync();
       if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 1);
-      // (B) look back
+      // (B) deterministic fixed-depth look-back: c_in(b) composes the
+      // aggregates of the kLB blocks b-1 .. b-kLB (fixed order, newest first)
+      // onto the INCLUSIVE carry of block b-kLB-1 (or c_0).  The arithmetic
+      // never depends on timing, so results are run-to-run and
+      // chunking/GPU-count invariant; the inclusive chain advances kLB+1
+      // blocks per hop.
       float cin;
       {
-        float Aacc = 1.f, Bacc = 0.f;  // map from c after block j to c after block b-1
-        int j = b - 1;
-        while (true) {
-          if (j < 0) {
-            cin = Aacc * ld_cg(&a.cbuf[unit]) + Bacc;
-            break;
-          }
-          if (et == 0) {
-            int st;
-            while ((st = ld_acquire(&a.status[(size_t)j * a.nU + u])) == 0) __nanosleep(32);
-            s_status = st;
-          }
-          tc_epi_sync();
-          const int st = s_status;
-          tc_epi_sync();
+        const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
+        // lanes of the first epilogue warp wait for the statuses in parallel
+        if (et < 32) {
+          const int j = b - 1 - et;
+          if (j >= jlo) while (ld_acquire(&a.status[(size_t)j * a.nU + u]) < 1) __nanosleep(32);
+          const int jb = jlo - 1;  // block whose inclusive carry anchors the chain
+          if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < 2) __nanosleep(32);
+        }
+        tc_epi_sync();
+        float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
+        for (int j = b - 1; j >= jlo; --j) {
           const size_t jidx = (size_t)j * a.Hpad + unit;
-          if (st == 2) {
-            cin = Aacc * ld_cg(&a.incl[jidx]) + Bacc;
-            break;
-          }
           const float Aj = ld_cg(&a.aggA[jidx]), Bj = ld_cg(&a.aggB[jidx]);
           Bacc = Aacc * Bj + Bacc;
           Aacc = Aacc * Aj;
-          --j;
         }
+        const float anchor = jlo > 0 ? ld_cg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit]) : ld_cg(&a.cbuf[unit]);
+        cin = Aacc * anchor + Bacc;
       }
       a.incl[sidx] = Ablk * cin + Bblk;
       __threadfence();

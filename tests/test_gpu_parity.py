@@ -394,3 +394,16 @@ def test_tensor_core_streaming_carry(P, oracle):
     assert st.query(9) == 1
     assert normwise(np.concatenate([a, b]), whole) <= 1e-6
     st.close()
+
+
+def test_tensor_core_look_back_is_deterministic(P, oracle):
+    """Fixed-depth look-back: bitwise identical results run to run (the
+    reference's worker-count invariance, test_blocked.py:386-396)."""
+    import torch
+    layers = oracle.generate_layers("qrnn", 512, 512, 1, 47, np.float32)
+    X = torch.from_numpy(np.random.default_rng(11).standard_normal((4096, 512)).astype(np.float32)).cuda()
+    st = P.DeviceStack("qrnn", layers, mode="bf16")
+    a = st.forward(X, 16).cpu().numpy()
+    for _ in range(3):
+        assert st.forward(X, 16).cpu().numpy().tobytes() == a.tobytes()
+    st.close()
