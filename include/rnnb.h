@@ -74,6 +74,16 @@ rnnb_status rnnb_plan_blocks(int64_t seq_len, int64_t block_size, int64_t* n_blo
  * d_in == d_h (cells.py:89). */
 rnnb_status rnnb_stack_create(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
                               const int64_t* d_h, int mode, int device);
+/* As rnnb_stack_create, with flags: RNNB_FLAG_WIDE_SRU accepts SRU layers
+ * with d_in > d_h whose highway term reads the input columns
+ * [hw_off, hw_off + d_h) (rnnb_stack_set_highway) and does not require
+ * layer widths to chain (hidden-dimension sharding: each rank owns d_h/G
+ * units of a layer that reads the full all-gathered input).  The reference
+ * cannot express this (cells.py:89); BASELINE cfg5 needs it. */
+#define RNNB_FLAG_WIDE_SRU 1
+rnnb_status rnnb_stack_create_ex(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
+                                 const int64_t* d_h, int mode, int device, int flags);
+rnnb_status rnnb_stack_set_highway(rnnb_stack_t h, int layer, int64_t col_offset);
 rnnb_status rnnb_stack_destroy(rnnb_stack_t h);
 
 /* Upload one layer.  mats[] are HOST row-major arrays in the reference's

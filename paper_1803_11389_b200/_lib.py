@@ -20,8 +20,10 @@ DT_F32, DT_F64 = 0, 1
 SYMBOLS = (
     "rnnb_last_error", "rnnb_version", "rnnb_plan_blocks", "rnnb_stack_create",
     "rnnb_stack_destroy", "rnnb_stack_set_layer", "rnnb_forward", "rnnb_forward_host",
-    "rnnb_gates", "rnnb_sweep", "rnnb_finalize", "rnnb_query",
+    "rnnb_gates", "rnnb_sweep", "rnnb_finalize", "rnnb_query", "rnnb_stack_create_ex",
+    "rnnb_stack_set_highway",
 )
+FLAG_WIDE_SRU = 1
 
 _lib = None
 
@@ -47,6 +49,8 @@ def load():
         "rnnb_plan_blocks": ([i64, i64, P64, P64], ci),
         "rnnb_stack_create": ([ctypes.POINTER(vp), ci, ci, P64, P64, ci, ci], ci),
         "rnnb_stack_destroy": ([vp], ci),
+        "rnnb_stack_create_ex": ([ctypes.POINTER(vp), ci, ci, P64, P64, ci, ci, ci], ci),
+        "rnnb_stack_set_highway": ([vp, ci, i64], ci),
         "rnnb_stack_set_layer": ([vp, ci, ctypes.POINTER(vp), ci, ci], ci),
         "rnnb_forward": ([vp, vp, i64, i64, i64, vp, i64, vp, vp, vp], ci),
         "rnnb_forward_host": ([vp, vp, i64, i64, vp, vp, vp, vp], ci),

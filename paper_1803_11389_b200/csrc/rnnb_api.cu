@@ -45,6 +45,7 @@ struct Layer {
   int Hpad128 = 0;
   bool last_tc = false;
   float* bias_tc = nullptr;  // [Hpad128][2]
+  int64_t hw_off = 0;        // SRU highway reads x[:, hw_off + unit] (wide / sharded SRU)
 };
 
 }  // namespace
@@ -161,7 +162,7 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)nB * nU * sizeof(int), s));
   if (c_io) CUDA_TRY(cudaMemcpyAsync(h->cbuf, c_io, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
   TcArgs a{};
-  a.Xhw = X;
+  a.Xhw = X + ly.hw_off;
   a.ldhw = ldx;
   a.Hout = Hout;
   a.ldh = ldh;
@@ -211,7 +212,7 @@ rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_
   a.X = X;
   a.ldx = ldx;
   a.xcarry = h->kind == RNNB_QRNN ? xc_io : nullptr;
-  a.Xhw = X;
+  a.Xhw = X + ly.hw_off;
   a.ldhw = ldx;
   a.Hout = Hout;
   a.ldh = ldh;
@@ -314,6 +315,12 @@ rnnb_status rnnb_plan_blocks(int64_t seq_len, int64_t block_size, int64_t* n_blo
 
 rnnb_status rnnb_stack_create(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
                               const int64_t* d_h, int mode, int device) {
+  return rnnb_stack_create_ex(out, kind, n_layers, d_in, d_h, mode, device, 0);
+}
+
+rnnb_status rnnb_stack_create_ex(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
+                                 const int64_t* d_h, int mode, int device, int flags) {
+  const bool wide = (flags & RNNB_FLAG_WIDE_SRU) != 0;
   if (!out) return fail(RNNB_EINVAL, "out is null");
   *out = nullptr;
   if (kind != RNNB_SRU && kind != RNNB_QRNN)
@@ -323,8 +330,9 @@ rnnb_status rnnb_stack_create(rnnb_stack_t* out, int kind, int n_layers, const i
   if (!d_in || !d_h) return fail(RNNB_EINVAL, "null dimension arrays");
   for (int l = 0; l < n_layers; ++l) {
     if (d_in[l] < 1 || d_h[l] < 1) return fail(RNNB_EINVAL, "d_in and d_h must be >= 1");
-    if (kind == RNNB_SRU && d_in[l] != d_h[l]) return fail(RNNB_EINVAL, "SRU requires d_in == d_h");
-    if (l > 0 && d_in[l] != d_h[l - 1])
+    if (kind == RNNB_SRU && !wide && d_in[l] != d_h[l]) return fail(RNNB_EINVAL, "SRU requires d_in == d_h");
+    if (kind == RNNB_SRU && wide && d_in[l] < d_h[l]) return fail(RNNB_EINVAL, "wide SRU needs d_in >= d_h");
+    if (l > 0 && !wide && d_in[l] != d_h[l - 1])
       return fail(RNNB_EINVAL, "layer " + std::to_string(l) + " input width does not match previous layer width");
     if (d_in[l] > (1 << 24) || d_h[l] > (1 << 24)) return fail(RNNB_EUNSUPPORTED, "dimension too large");
   }
@@ -463,6 +471,16 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
   }
   ly.loaded = true;
   cudaSetDevice(cur);
+  return RNNB_OK;
+}
+
+rnnb_status rnnb_stack_set_highway(rnnb_stack_t h, int layer, int64_t col_offset) {
+  if (!h) return fail(RNNB_EINVAL, "null stack handle");
+  if (layer < 0 || layer >= h->n_layers) return fail(RNNB_EINVAL, "layer index out of range");
+  if (h->kind != RNNB_SRU) return fail(RNNB_EINVAL, "highway offset applies to SRU layers");
+  Layer& ly = h->layers[layer];
+  if (col_offset < 0 || col_offset + ly.dh > ly.din) return fail(RNNB_EINVAL, "highway columns out of range");
+  ly.hw_off = col_offset;
   return RNNB_OK;
 }
 

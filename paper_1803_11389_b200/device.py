@@ -54,7 +54,7 @@ class DeviceStack:
     "tf32" (weights and x rounded to tf32 at the product).
     """
 
-    def __init__(self, kind, layers, mode="f32", device=None):
+    def __init__(self, kind, layers, mode="f32", device=None, wide=False, highway_offsets=None):
         torch = _torch()
         if not torch.cuda.is_available():
             raise _lib.RnnbError("CUDA is not available: the blocked path has no CPU fallback")
@@ -73,11 +73,14 @@ class DeviceStack:
         din = (ctypes.c_int64 * n)(*self.d_in)
         dh = (ctypes.c_int64 * n)(*self.d_h)
         h = ctypes.c_void_p()
-        _lib.check(self.lib.rnnb_stack_create(ctypes.byref(h), self.kind, n, din, dh,
-                                              _lib.MODES[mode], self.device))
+        flags = _lib.FLAG_WIDE_SRU if wide else 0
+        _lib.check(self.lib.rnnb_stack_create_ex(ctypes.byref(h), self.kind, n, din, dh,
+                                                 _lib.MODES[mode], self.device, flags))
         self._h = h
         for li, m in enumerate(mats):
             self.set_layer(li, m)
+        for li, off in enumerate(highway_offsets or []):
+            _lib.check(self.lib.rnnb_stack_set_highway(self._h, li, int(off)))
 
     @property
     def n_layers(self):
