@@ -118,7 +118,7 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
     """Dominant kernel = the fused layer kernel (one launch per layer)."""
     L = w.seq_len
     flops = workloads.flops_per_step(w) * L / launches_per_step
-    s_w = {"f32": 4, "tf32": 4, "bf16": 2, "f64": 8}[mode]
+    s_w = {"f32": 4, "tf32": 4, "bf16": 2, "f64": 8, "f32x3": 8}[mode]
     s_a = 8 if mode == "f64" else 4
     params = workloads.param_count(w)
     nblocks = -(-L // T_b)
@@ -142,13 +142,15 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
             src += " x 0.5 (fp64 rate)"
         pipe = "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)"
     else:
-        peak = pk["bf16_tflops"] * (0.5 if mode == "tf32" else 1.0)
+        peak = pk["bf16_tflops"] * (0.5 if mode in ("tf32", "f32x3") else 1.0)
         pipe = "tcgen05 " + mode
-        src = "MEASURED_PEAKS.json bf16_tflops" + (" x 0.5 (tf32)" if mode == "tf32" else "")
+        src = "MEASURED_PEAKS.json bf16_tflops" + (" x 0.5 (tf32 rate)" if mode in ("tf32", "f32x3") else "")
+        if mode == "f32x3":
+            src += "; algorithmic FLOPs only (3 tf32 products per fp32 product executed)"
     achieved = flops / sec / 1e12
     hbm = pk["hbm_gbs"]
     return {
-        "bound": "tensor" if mode in ("bf16", "tf32") else "compute",
+        "bound": "tensor" if mode in ("bf16", "tf32", "f32x3") else "compute",
         "pipe": pipe,
         "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
         "frac": round(achieved / peak, 4), "peak_source": src,
@@ -401,7 +403,7 @@ def main():
     ap.add_argument("--block", type=int, default=32)
     ap.add_argument("--mode", default="f32", choices=("f32", "f64", "bf16", "tf32"))
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
-    ap.add_argument("--extra-modes", default="bf16,tf32",
+    ap.add_argument("--extra-modes", default="bf16,tf32,f32x3",
                     help="tensor-core numerics modes timed beside the headline mode")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-sample", type=int, default=512, help="time steps in the CPU sample")

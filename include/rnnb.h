@@ -55,8 +55,11 @@ typedef enum { RNNB_SRU = 1, RNNB_QRNN = 2 } rnnb_cell;
 /* Compute modes.  F32/F64 match the reference's precisions (kernels.py:25)
  * with accumulators of the element type.  BF16 stores weights as bf16 and
  * rounds x to bf16 at the product (fp32 accumulate, fp32 gates/state/h);
- * TF32 rounds weights and x to tf32 at the product (fp32 accumulate). */
-typedef enum { RNNB_F32 = 0, RNNB_F64 = 1, RNNB_BF16 = 2, RNNB_TF32 = 3 } rnnb_mode;
+ * TF32 rounds weights and x to tf32 at the product (fp32 accumulate).
+ * F32X3: fp32 inputs, products split 3xTF32 on the tensor cores
+ * (a_hi b_hi + a_hi b_lo + a_lo b_hi, fp32 accumulate) for 16 <= T_b <= 64,
+ * exact fp32 FFMA below that. */
+typedef enum { RNNB_F32 = 0, RNNB_F64 = 1, RNNB_BF16 = 2, RNNB_TF32 = 3, RNNB_F32X3 = 4 } rnnb_mode;
 
 typedef enum { RNNB_DT_F32 = 0, RNNB_DT_F64 = 1 } rnnb_dtype;
 

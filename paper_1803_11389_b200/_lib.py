@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "librnnb.so")
 
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4
 SRU, QRNN = 1, 2
-MODES = {"f32": 0, "f64": 1, "bf16": 2, "tf32": 3}
+MODES = {"f32": 0, "f64": 1, "bf16": 2, "tf32": 3, "f32x3": 4}
 DT_F32, DT_F64 = 0, 1
 
 # every symbol include/rnnb.h declares (checked by tests/test_abi.py)

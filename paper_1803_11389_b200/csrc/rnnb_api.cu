@@ -124,18 +124,24 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
 }
 
 bool use_tc(const rnnb_stack* h, int64_t Tb) {
-  return (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) && Tb >= 16 && Tb <= 128 &&
-         getenv("RNNB_NO_TC") == nullptr;
+  if (getenv("RNNB_NO_TC") != nullptr || Tb < 16) return false;
+  if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) return Tb <= 128;
+  if (h->mode == RNNB_F32X3) return Tb <= 64;
+  return false;
+}
+
+int tc_mode_of(int mode) {
+  return mode == RNNB_BF16 ? TC_BF16 : (mode == RNNB_TF32 ? TC_TF32 : TC_3XTF32);
 }
 
 // one layer on the tcgen05 path (tc_layer.cuh)
 rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb, float* Hout,
                             int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
   Layer& ly = h->layers[li];
-  const int mode = h->mode == RNNB_BF16 ? TC_BF16 : TC_TF32;
+  const int mode = tc_mode_of(h->mode);
   const int es = mode == TC_BF16 ? 2 : 4;
   const int64_t ldop = (ly.din + 7) / 8 * 8;
-  const size_t opb = (size_t)(L + 1) * ldop * es;
+  const size_t opb = (size_t)(mode == TC_3XTF32 ? 2 : 1) * (L + 1) * ldop * es;
   if (h->op_bytes < opb) {
     if (h->op) cudaFree(h->op);
     h->op = nullptr;
@@ -326,7 +332,7 @@ rnnb_status rnnb_stack_create_ex(rnnb_stack_t* out, int kind, int n_layers, cons
   if (kind != RNNB_SRU && kind != RNNB_QRNN)
     return fail(RNNB_EINVAL, "blocked execution covers SRU and QRNN; use lstm_run_precomputed for LSTM");
   if (n_layers < 1) return fail(RNNB_EINVAL, "n_layers must be >= 1");
-  if (mode < RNNB_F32 || mode > RNNB_TF32) return fail(RNNB_EINVAL, "unknown compute mode");
+  if (mode < RNNB_F32 || mode > RNNB_F32X3) return fail(RNNB_EINVAL, "unknown compute mode");
   if (!d_in || !d_h) return fail(RNNB_EINVAL, "null dimension arrays");
   for (int l = 0; l < n_layers; ++l) {
     if (d_in[l] < 1 || d_h[l] < 1) return fail(RNNB_EINVAL, "d_in and d_h must be >= 1");
@@ -437,14 +443,16 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
     CUDA_TRY(cudaMemcpy(ly.bias, b.data(), b.size(), cudaMemcpyHostToDevice));
     ly.wbytes += b.size();
   }
-  if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) {
-    // tensor-core layout: rows g*Hpad128 + u (gate-major), columns [tap][Dtc]
+  if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32 || h->mode == RNNB_F32X3) {
+    // tensor-core layout: rows (p*3 + g)*Hpad128 + u (plane p: hi / lo for
+    // 3xTF32, gate-major), columns [tap][Dtc]
     const int KT = h->mode == RNNB_BF16 ? 64 : 32;
+    const int planes = h->mode == RNNB_F32X3 ? 2 : 1;
     const int64_t Dtc = (ly.din + KT - 1) / KT * KT;
     ly.Hpad128 = (int)((ly.dh + 127) / 128 * 128);
     ly.tcKp = (int)(T * Dtc);
     const size_t rows_tc = (size_t)3 * ly.Hpad128;
-    std::vector<unsigned char> tc(rows_tc * ly.tcKp * ws, 0);
+    std::vector<unsigned char> tc(planes * rows_tc * ly.tcKp * ws, 0);
     for (int g = 0; g < 3; ++g)
       for (int64_t u = 0; u < ly.dh; ++u)
         for (int tap = 0; tap < T; ++tap) {
@@ -452,8 +460,15 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
           for (int64_t k = 0; k < ly.din; ++k) {
             const float v = (float)get(m, u * ly.din + k);
             const size_t dst = ((size_t)g * ly.Hpad128 + u) * ly.tcKp + (size_t)tap * Dtc + k;
-            if (h->mode == RNNB_BF16) reinterpret_cast<uint16_t*>(tc.data())[dst] = to_bf16(v);
-            else reinterpret_cast<float*>(tc.data())[dst] = to_tf32(v);
+            if (h->mode == RNNB_BF16) {
+              reinterpret_cast<uint16_t*>(tc.data())[dst] = to_bf16(v);
+            } else if (h->mode == RNNB_TF32) {
+              reinterpret_cast<float*>(tc.data())[dst] = to_tf32(v);
+            } else {
+              const float hi = to_tf32(v);
+              reinterpret_cast<float*>(tc.data())[dst] = hi;
+              reinterpret_cast<float*>(tc.data())[dst + rows_tc * ly.tcKp] = to_tf32(v - hi);
+            }
           }
         }
     if (ly.Wtc) cudaFree(ly.Wtc), ly.Wtc = nullptr;

@@ -15,5 +15,6 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
                          int num_sms, cudaStream_t s, int* grid_out);
 
 int tc_pick_n(int T_b);
+int tc_max_n(int mode);
 
 }  // namespace rnnb

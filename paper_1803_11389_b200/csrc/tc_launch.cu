@@ -15,10 +15,15 @@ __global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, cons
     const int64_t r = i / D;
     const int d = (int)(i - r * D);
     const float v = r == 0 ? (xcarry ? xcarry[d] : 0.f) : X[(r - 1) * ldx + d];
-    if (MODE == TC_BF16)
+    if (MODE == TC_BF16) {
       reinterpret_cast<__nv_bfloat16*>(out)[r * ldo + d] = __float2bfloat16_rn(v);
-    else
+    } else if (MODE == TC_TF32) {
       reinterpret_cast<float*>(out)[r * ldo + d] = round_x(v, XR_TF32);
+    } else {  // 3xTF32: hi plane rows [0, L], lo plane rows [L+1, 2L+1]
+      const float hi = round_x(v, XR_TF32);
+      reinterpret_cast<float*>(out)[r * ldo + d] = hi;
+      reinterpret_cast<float*>(out)[(r + L + 1) * ldo + d] = round_x(v - hi, XR_TF32);
+    }
   }
 }
 
@@ -28,7 +33,8 @@ cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xc
   const int bs = 256;
   const int grid = (int)((n + bs - 1) / bs < 148 * 16 ? (n + bs - 1) / bs : 148 * 16);
   if (mode == TC_BF16) to_operand_kernel<TC_BF16><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
-  else to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
+  else if (mode == TC_TF32) to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
+  else to_operand_kernel<TC_3XTF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
   return cudaGetLastError();
 }
 
@@ -60,6 +66,8 @@ static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUten
   return cudaGetLastError();
 }
 
+int tc_max_n(int mode) { return mode == TC_3XTF32 ? 64 : 128; }
+
 int tc_pick_n(int T_b) {
   if (T_b <= 16) return 16;
   if (T_b <= 32) return 32;
@@ -74,7 +82,9 @@ static cudaError_t run_n(int N, const TcArgs& a, const CUtensorMap& tw, const CU
     case 16: return launch_tc<CELL, MODE, 16>(a, tw, tx, grid, s);
     case 32: return launch_tc<CELL, MODE, 32>(a, tw, tx, grid, s);
     case 64: return launch_tc<CELL, MODE, 64>(a, tw, tx, grid, s);
-    default: return launch_tc<CELL, MODE, 128>(a, tw, tx, grid, s);
+    default:
+      if constexpr (MODE == TC_3XTF32) return cudaErrorInvalidValue;  // stages would not fit
+      else return launch_tc<CELL, MODE, 128>(a, tw, tx, grid, s);
   }
 }
 
@@ -83,22 +93,25 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
   const int N = tc_pick_n(a.T_b);
   const int es = mode == TC_BF16 ? 2 : 4;
   const int KT = mode == TC_BF16 ? 64 : 32;
+  const int planes = mode == TC_3XTF32 ? 2 : 1;
   const CUtensorMapDataType dt = mode == TC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   CUtensorMap tw, tx;
-  if (!make_map(&tw, dt, es, Wtc, (uint64_t)Kp, (uint64_t)3 * a.Hpad, (uint64_t)Kp, KT, 128))
+  if (!make_map(&tw, dt, es, Wtc, (uint64_t)Kp, (uint64_t)3 * planes * a.Hpad, (uint64_t)Kp, KT, 128))
     return cudaErrorInvalidValue;
-  // operand X has L+1 rows (row 0 = x_{-1}); the kernel addresses row t+1
-  if (!make_map(&tx, dt, es, Xop, (uint64_t)a.D, (uint64_t)(a.L + 1), (uint64_t)ldop_in, KT, N))
+  // operand X has L+1 rows per plane (row 0 = x_{-1}); the kernel addresses row t+1
+  if (!make_map(&tx, dt, es, Xop, (uint64_t)a.D, (uint64_t)planes * (a.L + 1), (uint64_t)ldop_in, KT, N))
     return cudaErrorInvalidValue;
   const int nitems = a.nU * a.nB;
   const int grid = nitems < num_sms ? nitems : num_sms;
   if (grid_out) *grid_out = grid;
   if (cell == SRU) {
     if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tw, tx, grid, s);
-    return run_n<SRU, TC_TF32>(N, a, tw, tx, grid, s);
+    if (mode == TC_TF32) return run_n<SRU, TC_TF32>(N, a, tw, tx, grid, s);
+    return run_n<SRU, TC_3XTF32>(N, a, tw, tx, grid, s);
   }
   if (mode == TC_BF16) return run_n<QRNN, TC_BF16>(N, a, tw, tx, grid, s);
-  return run_n<QRNN, TC_TF32>(N, a, tw, tx, grid, s);
+  if (mode == TC_TF32) return run_n<QRNN, TC_TF32>(N, a, tw, tx, grid, s);
+  return run_n<QRNN, TC_3XTF32>(N, a, tw, tx, grid, s);
 }
 
 }  // namespace rnnb

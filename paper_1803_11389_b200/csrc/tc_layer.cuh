@@ -33,7 +33,9 @@
 
 namespace rnnb {
 
-enum TcMode : int { TC_BF16 = 0, TC_TF32 = 1 };
+// TC_3XTF32: fp32-accurate split products on the tf32 pipe,
+//   a.b ~= a_hi.b_hi + a_hi.b_lo + a_lo.b_hi  (hi = tf32(x), lo = tf32(x - hi))
+enum TcMode : int { TC_BF16 = 0, TC_TF32 = 1, TC_3XTF32 = 2 };
 
 struct TcArgs {
   const float* Xhw;   // SRU highway source x (fp32, raw), row stride ldhw
@@ -70,6 +72,7 @@ template <> struct TcT<TC_TF32> {
   static constexpr int UK = 8;   // K per tcgen05.mma (kind::tf32)
   static constexpr uint32_t FMT = 2;  // TF32
 };
+template <> struct TcT<TC_3XTF32> : TcT<TC_TF32> {};
 
 constexpr int kTcThreads = 192;
 constexpr int kLB = 32;  // look-back depth (aggregates composed per block)
@@ -171,8 +174,11 @@ struct TcCfg {
   static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
   static constexpr int A_BYTES = 128 * 128;  // one gate tile: 128 rows x 128 B
   static constexpr int B_BYTES = N * 128;
-  static constexpr int STAGE_BYTES = 3 * A_BYTES + B_BYTES;
-  static constexpr int STAGES = (4 * STAGE_BYTES + 2048 <= 227 * 1024) ? 4 : 3;
+  static constexpr int SPLIT = MODE == TC_3XTF32 ? 2 : 1;  // hi (+ lo) planes per operand
+  static constexpr int STAGE_BYTES = SPLIT * (3 * A_BYTES + B_BYTES);
+  static constexpr int STAGES = (4 * STAGE_BYTES + 2048 <= 227 * 1024)   ? 4
+                                : (3 * STAGE_BYTES + 2048 <= 227 * 1024) ? 3
+                                                                          : 2;
   static constexpr int ACC_COLS = 3 * N;
   static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;
   static constexpr int TMEM_COLS = (NACC * ACC_COLS <= 32) ? 32 : (NACC * ACC_COLS <= 64) ? 64
@@ -224,12 +230,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait_sleep(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
-          for (int g = 0; g < 3; ++g)
-            tma_load_2d(st + g * C::A_BYTES, &tmW, kt * C::KT, g * a.Hpad + u * 128, &full[s]);
           const int tap = kt >= a.nKtap ? 1 : 0;
           const int kx = (kt - tap * a.nKtap) * C::KT;
-          // operand row r holds x_{r-1}: block rows t0.. for tap 0, t0-1.. for tap 1
-          tma_load_2d(st + 3 * C::A_BYTES, &tmX, kx, t0 + 1 - tap, &full[s]);
+#pragma unroll
+          for (int p = 0; p < C::SPLIT; ++p) {  // hi plane, then lo plane (3xTF32)
+            unsigned char* sp = st + p * (3 * C::A_BYTES + C::B_BYTES);
+            for (int g = 0; g < 3; ++g)
+              tma_load_2d(sp + g * C::A_BYTES, &tmW, kt * C::KT, (p * 3 + g) * a.Hpad + u * 128, &full[s]);
+            // operand row r holds x_{r-1}: block rows t0.. for tap 0, t0-1.. for tap 1
+            tma_load_2d(sp + 3 * C::A_BYTES, &tmX, kx, (int)(p * (a.L + 1)) + t0 + 1 - tap, &full[s]);
+          }
         }
       }
     }
@@ -249,6 +259,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc_fence_after();
           unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
           const uint64_t bdesc0 = sw128_desc(st + 3 * C::A_BYTES);
+          constexpr int HALF = 3 * C::A_BYTES + C::B_BYTES;
 #pragma unroll
           for (int g = 0; g < 3; ++g) {
             const uint64_t adesc0 = sw128_desc(st + g * C::A_BYTES);
@@ -256,7 +267,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             for (int kk = 0; kk < C::KT / C::UK; ++kk) {
               // advance the start address along K inside the 128-B swizzle row
               const uint64_t koff = (uint64_t)((kk * C::UK * C::ES) >> 4);
-              tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kt | kk) != 0);
+              if (C::SPLIT == 2) {
+                const uint64_t blo = sw128_desc(st + HALF + 3 * C::A_BYTES) + koff;
+                const uint64_t alo = sw128_desc(st + HALF + g * C::A_BYTES) + koff;
+                tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kt | kk) != 0);
+                tc_mma<MODE>(dbase + g * N, adesc0 + koff, blo, idesc, 1);
+                tc_mma<MODE>(dbase + g * N, alo, bdesc0 + koff, idesc, 1);
+              } else {
+                tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kt | kk) != 0);
+              }
             }
           }
           tc_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
