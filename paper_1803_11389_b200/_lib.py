@@ -9,7 +9,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librnnb.so")
+LIB_PATH = os.environ.get("RNNB_LIB", os.path.join(HERE, "librnnb.so"))  # override for A/B timing only
 
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4
 SRU, QRNN = 1, 2

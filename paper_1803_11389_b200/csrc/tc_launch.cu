@@ -51,30 +51,19 @@ static bool make_map(CUtensorMap* tm, CUtensorMapDataType dt, int es, const void
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int CELL, int MODE, int N, int CL>
+template <int CELL, int MODE, int N>
 static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx, int grid,
                              cudaStream_t s) {
   using C = TcCfg<MODE, N>;
-  auto k = tc_layer_kernel<CELL, MODE, N, CL>;
+  auto k = tc_layer_kernel<CELL, MODE, N>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = C::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CL;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k, a, tw, tx);
+  k<<<grid, kTcThreads, C::SMEM, s>>>(a, tw, tx);
+  return cudaGetLastError();
 }
 
 int tc_max_n(int mode) { return mode == TC_3XTF32 ? 64 : 128; }
@@ -86,24 +75,17 @@ int tc_pick_n(int T_b) {
   return 128;
 }
 
-template <int CELL, int MODE, int CL>
+template <int CELL, int MODE>
 static cudaError_t run_n(int N, const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx, int grid,
                          cudaStream_t s) {
   switch (N) {
-    case 16: return launch_tc<CELL, MODE, 16, CL>(a, tw, tx, grid, s);
-    case 32: return launch_tc<CELL, MODE, 32, CL>(a, tw, tx, grid, s);
-    case 64: return launch_tc<CELL, MODE, 64, CL>(a, tw, tx, grid, s);
+    case 16: return launch_tc<CELL, MODE, 16>(a, tw, tx, grid, s);
+    case 32: return launch_tc<CELL, MODE, 32>(a, tw, tx, grid, s);
+    case 64: return launch_tc<CELL, MODE, 64>(a, tw, tx, grid, s);
     default:
       if constexpr (MODE == TC_3XTF32) return cudaErrorInvalidValue;  // stages would not fit
-      else return launch_tc<CELL, MODE, 128, CL>(a, tw, tx, grid, s);
+      else return launch_tc<CELL, MODE, 128>(a, tw, tx, grid, s);
   }
-}
-
-template <int CELL, int MODE>
-static cudaError_t run_cl(int N, int CL, const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx,
-                          int grid, cudaStream_t s) {
-  if (CL == 2) return run_n<CELL, MODE, 2>(N, a, tw, tx, grid, s);
-  return run_n<CELL, MODE, 1>(N, a, tw, tx, grid, s);
 }
 
 cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, const void* Xop, int64_t ldop_in,
@@ -114,28 +96,22 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
   const int planes = mode == TC_3XTF32 ? 2 : 1;
   const CUtensorMapDataType dt = mode == TC_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
   CUtensorMap tw, tx;
-  // Optional (RNNB_TC_MC=1): weight tiles multicast across a 2-CTA cluster (each
-  // CTA loads 64 of the 128 rows).  Measured slower on B200 (cfg2 bf16 T_b=32:
-  // 19.2 vs 22.2 M steps/s): the pair runs in lockstep and L2 already
-  // de-duplicates near-simultaneous reads of the same tile, so it is off.
-  const int CL = (a.nB >= 2 && getenv("RNNB_TC_MC") != nullptr) ? 2 : 1;
-  if (!make_map(&tw, dt, es, Wtc, (uint64_t)Kp, (uint64_t)3 * planes * a.Hpad, (uint64_t)Kp, KT, 128 / CL))
+  if (!make_map(&tw, dt, es, Wtc, (uint64_t)Kp, (uint64_t)3 * planes * a.Hpad, (uint64_t)Kp, KT, 128))
     return cudaErrorInvalidValue;
   // operand X has L+1 rows per plane (row 0 = x_{-1}); the kernel addresses row t+1
   if (!make_map(&tx, dt, es, Xop, (uint64_t)a.D, (uint64_t)planes * (a.L + 1), (uint64_t)ldop_in, KT, N))
     return cudaErrorInvalidValue;
-  const int nslots = a.nU * ((a.nB + CL - 1) / CL);
-  const int max_ctas = num_sms / CL * CL;
-  const int grid = nslots * CL < max_ctas ? nslots * CL : max_ctas;
+  const int nitems = a.nU * a.nB;
+  const int grid = nitems < num_sms ? nitems : num_sms;
   if (grid_out) *grid_out = grid;
   if (cell == SRU) {
-    if (mode == TC_BF16) return run_cl<SRU, TC_BF16>(N, CL, a, tw, tx, grid, s);
-    if (mode == TC_TF32) return run_cl<SRU, TC_TF32>(N, CL, a, tw, tx, grid, s);
-    return run_cl<SRU, TC_3XTF32>(N, CL, a, tw, tx, grid, s);
+    if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tw, tx, grid, s);
+    if (mode == TC_TF32) return run_n<SRU, TC_TF32>(N, a, tw, tx, grid, s);
+    return run_n<SRU, TC_3XTF32>(N, a, tw, tx, grid, s);
   }
-  if (mode == TC_BF16) return run_cl<QRNN, TC_BF16>(N, CL, a, tw, tx, grid, s);
-  if (mode == TC_TF32) return run_cl<QRNN, TC_TF32>(N, CL, a, tw, tx, grid, s);
-  return run_cl<QRNN, TC_3XTF32>(N, CL, a, tw, tx, grid, s);
+  if (mode == TC_BF16) return run_n<QRNN, TC_BF16>(N, a, tw, tx, grid, s);
+  if (mode == TC_TF32) return run_n<QRNN, TC_TF32>(N, a, tw, tx, grid, s);
+  return run_n<QRNN, TC_3XTF32>(N, a, tw, tx, grid, s);
 }
 
 }  // namespace rnnb

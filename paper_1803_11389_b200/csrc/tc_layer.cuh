@@ -166,32 +166,6 @@ __device__ __forceinline__ float ld_cg(const float* p) {
   asm volatile("ld.global.cg.f32 %0, [%1];\n" : "=f"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-// 2-D TMA tile load multicast to every CTA of `mask` (same smem offsets; each
-// destination CTA's mbarrier at the same offset gets the complete_tx)
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-// commit: arrive on the mbarrier at this offset in every CTA of `mask`
-__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
-          smem_u32(bar)),
-      "h"(mask)
-      : "memory");
-}
 // named barrier 2 over the four epilogue warps
 __device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
 
@@ -212,13 +186,7 @@ struct TcCfg {
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-// CL = CTAs per cluster.  With CL == 2 the pair works on the same unit tile
-// for consecutive time blocks (2bb, 2bb+1): every weight tile is fetched
-// from L2 once per pair -- each CTA loads half of its rows and multicasts
-// them into both CTAs' shared memory -- while each CTA loads its own x tile.
-// A stage may be refilled only after BOTH CTAs' MMAs consumed it, so the
-// MMA commits arrive on the empty barriers of both CTAs.
-template <int CELL, int MODE, int N, int CL>
+template <int CELL, int MODE, int N>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_layer_kernel(TcArgs a, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX) {
   using C = TcCfg<MODE, N>;
@@ -231,16 +199,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // work slots: pair p = bb*nU + u covers blocks bb*CL + rank of unit tile u
-  const int rank = CL > 1 ? (int)cluster_rank() : 0;
-  const int nbb = (a.nB + CL - 1) / CL;
-  const int nslots = a.nU * nbb;
-  const int slot0 = blockIdx.x / CL, slot_step = gridDim.x / CL;
+  const int nitems = a.nU * a.nB;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CL);
+      mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&acc_full[i], 1);
@@ -251,7 +215,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 1) tmem_alloc(tmem_base_smem, C::TMEM_COLS);
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync_all();  // peers' barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tmem = *tmem_base_smem;
 
@@ -259,9 +222,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       uint32_t it = 0;
-      for (int sl = slot0; sl < nslots; sl += slot_step) {
-        const int bb = sl / a.nU, u = sl - (sl / a.nU) * a.nU;
-        const int b = bb * CL + rank;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
         const int t0 = b * a.T_b;
         for (int kt = 0; kt < a.nK; ++kt, ++it) {
           const int s = it % C::STAGES;
@@ -273,14 +235,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
           for (int p = 0; p < C::SPLIT; ++p) {  // hi plane, then lo plane (3xTF32)
             unsigned char* sp = st + p * (3 * C::A_BYTES + C::B_BYTES);
-            for (int g = 0; g < 3; ++g) {
-              const int row0 = (p * 3 + g) * a.Hpad + u * 128;
-              if (CL == 1)
-                tma_load_2d(sp + g * C::A_BYTES, &tmW, kt * C::KT, row0, &full[s]);
-              else  // my half of the rows, into both CTAs
-                tma_load_2d_mc(sp + g * C::A_BYTES + rank * (C::A_BYTES / CL), &tmW, kt * C::KT,
-                               row0 + rank * (128 / CL), &full[s], (uint16_t)((1u << CL) - 1));
-            }
+            for (int g = 0; g < 3; ++g)
+              tma_load_2d(sp + g * C::A_BYTES, &tmW, kt * C::KT, (p * 3 + g) * a.Hpad + u * 128, &full[s]);
             // operand row r holds x_{r-1}: block rows t0.. for tap 0, t0-1.. for tap 1
             tma_load_2d(sp + 3 * C::A_BYTES, &tmX, kx, (int)(p * (a.L + 1)) + t0 + 1 - tap, &full[s]);
           }
@@ -292,7 +248,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = tc_idesc<MODE>(128, N);
       uint32_t it = 0, acc_it = 0;
-      for (int sl = slot0; sl < nslots; sl += slot_step, ++acc_it) {
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
         const int ab = acc_it % C::NACC;
         mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
         tc_fence_after();
@@ -322,9 +278,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               }
             }
           }
-          // frees the smem stage (in both CTAs of the pair) once these MMAs have read it
-          if (CL == 1) tc_commit(&empty[s]);
-          else tc_commit_mc(&empty[s], (uint16_t)((1u << CL) - 1));
+          tc_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
         }
         tc_commit(&acc_full[ab]);  // accumulators of this item complete
       }
@@ -342,15 +296,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int row = q * 32 + lane;          // unit within the tile
     const int et = threadIdx.x - 64;        // 0..127
     uint32_t acc_it = 0;
-    for (int sl = slot0; sl < nslots; sl += slot_step, ++acc_it) {
-      const int bb = sl / a.nU, u = sl - (sl / a.nU) * a.nU;
-      const int b = bb * CL + rank;
-      if (b >= a.nB) {  // padding slot of an odd block count: keep the pipeline in step
-        mbar_wait(&acc_full[acc_it % C::NACC], (acc_it / C::NACC) & 1);
-        tc_fence_before();
-        mbar_arrive(&acc_empty[acc_it % C::NACC]);
-        continue;
-      }
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
+      const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
       const int64_t t0 = (int64_t)b * a.T_b;
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       const int unit = u * 128 + row;
@@ -459,7 +406,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still multicast into it
   tc_fence_after();
   if (warp == 1) tmem_dealloc(tmem, C::TMEM_COLS);
 }

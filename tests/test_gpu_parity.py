@@ -435,18 +435,3 @@ def test_f32x3_split_tensor_core_meets_fp32_bound(P, oracle, kind):
     assert e3 <= 5e-5
     st.close()
     f32.close()
-
-
-def test_tensor_core_cluster_multicast_variant(P, oracle, monkeypatch):
-    """The 2-CTA weight-multicast variant (RNNB_TC_MC=1) computes the same
-    results as the unicast kernel (odd block count exercises the padding slot)."""
-    import torch
-    layers = oracle.generate_layers("sru", 384, 384, 1, 53, np.float32)
-    X = torch.from_numpy(np.random.default_rng(13).standard_normal((16 * 33 + 5, 384)).astype(np.float32)).cuda()
-    st = P.DeviceStack("sru", layers, mode="bf16")
-    a = st.forward(X, 16).cpu().numpy()
-    monkeypatch.setenv("RNNB_TC_MC", "1")
-    b = st.forward(X, 16).cpu().numpy()
-    assert st.query(9) == 1
-    assert a.tobytes() == b.tobytes()
-    st.close()
