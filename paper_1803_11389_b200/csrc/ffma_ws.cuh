@@ -82,6 +82,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// packed fp32x2 FMA (sm_100): d = a * b + c on (lo, hi) float pairs
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -310,11 +316,22 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       for (int p0 = 0; p0 < l; p0 += NT, ++pass) {
+        // fp32 with fp32 weights: packed FFMA2 (Blackwell fma.rn.f32x2) on
+        // (k even, k odd) accumulator pairs -- half the FMA issue slots; the
+        // pair halves are summed after the K loop
+        constexpr bool kPacked = sizeof(TA) == 4 && sizeof(TW) == 4 && XR == XR_NONE;
         TA acc[RH][CT];
+        unsigned long long acc2[kPacked ? RH : 1][kPacked ? CT : 1];
 #pragma unroll
         for (int r = 0; r < RH; ++r)
 #pragma unroll
           for (int ct = 0; ct < CT; ++ct) acc[r][ct] = TA(0);
+        if (kPacked) {
+#pragma unroll
+          for (int r = 0; r < (kPacked ? RH : 1); ++r)
+#pragma unroll
+            for (int ct = 0; ct < (kPacked ? CT : 1); ++ct) acc2[r][ct] = 0ull;
+        }
         for (int ch = 0; ch < nchunk; ++ch, ++seq) {
           const int s = seq % STAGES;
           if (!(a.dbg & 1)) mbar_wait(&full[s], (seq / STAGES) & 1);
@@ -328,27 +345,50 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             const TW* wl = Ws + ((size_t)(d0 / KV + kl) * Rs + rbase) * KV;
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap) {
-              TA xv[CT][KV];
-#pragma unroll
-              for (int ct = 0; ct < CT; ++ct) {
-                Vec16<TA> v = lds16<TA>(xl + (size_t)(LANES_T * ct - tap) * BXS);
-#pragma unroll
-                for (int e = 0; e < KV; ++e) xv[ct][e] = round_x(v.v[e], XR);
-              }
               const TW* wp = wl + (size_t)tap * (Dp / KV) * Rs * KV;
-#pragma unroll
-              for (int r = 0; r < RH; ++r) {
-                TA w[KV];
-                WLoad<TA, TW>::shared(wp + r * KV, w);
+              if constexpr (kPacked) {
+                ulonglong2 xp[CT];
 #pragma unroll
                 for (int ct = 0; ct < CT; ++ct)
+                  xp[ct] = *reinterpret_cast<const ulonglong2*>(xl + (size_t)(LANES_T * ct - tap) * BXS);
 #pragma unroll
-                  for (int e = 0; e < KV; ++e) acc[r][ct] = fma(w[e], xv[ct][e], acc[r][ct]);
+                for (int r = 0; r < RH; ++r) {
+                  const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(wp + r * KV);
+#pragma unroll
+                  for (int ct = 0; ct < CT; ++ct) {
+                    acc2[r][ct] = ffma2(w.x, xp[ct].x, acc2[r][ct]);
+                    acc2[r][ct] = ffma2(w.y, xp[ct].y, acc2[r][ct]);
+                  }
+                }
+              } else {
+                TA xv[CT][KV];
+#pragma unroll
+                for (int ct = 0; ct < CT; ++ct) {
+                  Vec16<TA> v = lds16<TA>(xl + (size_t)(LANES_T * ct - tap) * BXS);
+#pragma unroll
+                  for (int e = 0; e < KV; ++e) xv[ct][e] = round_x(v.v[e], XR);
+                }
+#pragma unroll
+                for (int r = 0; r < RH; ++r) {
+                  TA w[KV];
+                  WLoad<TA, TW>::shared(wp + r * KV, w);
+#pragma unroll
+                  for (int ct = 0; ct < CT; ++ct)
+#pragma unroll
+                    for (int e = 0; e < KV; ++e) acc[r][ct] = fma(w[e], xv[ct][e], acc[r][ct]);
+                }
               }
             }
           }
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if constexpr (kPacked) {
+#pragma unroll
+          for (int r = 0; r < RH; ++r)
+#pragma unroll
+            for (int ct = 0; ct < CT; ++ct)
+              acc[r][ct] = __uint_as_float((unsigned)acc2[r][ct]) + __uint_as_float((unsigned)(acc2[r][ct] >> 32));
         }
 #pragma unroll
         for (int r = 0; r < RH; ++r)
