@@ -1,0 +1,116 @@
+"""Time every BASELINE.json config on one GPU (beside bench.py's headline).
+
+    python tools/bench_configs.py [--reps 3] [--out profiles/configs_r1.json]
+
+Per config, mode and T_b: W=3 warm-up forwards, then `reps` forwards, each
+bracketed by CUDA events with a 256 MB L2 flush before it; steps/s = L /
+mean time.  cfg1-cfg4 run the blocked stack (DeviceStack; cfg3 adds the
+120->1024 projection and 1024->2000 logits), cfg5 runs the bidirectional
+wide SRU through partition.ShardedBidirSRU at world size 1 (all units on
+this GPU).  Outputs are not re-verified here (tests/ do that).
+"""
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+import paper_1803_11389_b200 as P  # noqa: E402
+from paper_1803_11389_b200 import partition, workloads  # noqa: E402
+from paper_1803_11389_b200.acoustic import AcousticSRU  # noqa: E402
+
+PLAN = {
+    "cfg1": [("f32", (1, 4, 16))],
+    "cfg2": [("f32", (1, 2, 4, 8, 16, 32, 64)), ("bf16", (16, 32, 64)), ("tf32", (16, 32, 64)),
+             ("f32x3", (16, 32, 64))],
+    "cfg3": [("f32", (1, 8, 32)), ("bf16", (1, 8, 32)), ("tf32", (8, 32))],
+    "cfg4": [("bf16", (32,)), ("f32", (32,))],
+    "cfg5": [("bf16", (16, 64))],
+}
+
+
+def timed(fn, reps, flush):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for i in range(reps):
+        flush.fill_(float(i))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return sum(ts) / len(ts)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--configs", default="cfg1,cfg2,cfg3,cfg4,cfg5")
+    ap.add_argument("--out", default=os.path.join(REPO, "profiles", "configs_r1.json"))
+    a = ap.parse_args()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    res = {}
+    pg = False
+    for name in a.configs.split(","):
+        t0 = time.time()
+        w = workloads.make(name)
+        X = torch.from_numpy(w.X).cuda()
+        L = w.seq_len
+        fl = workloads.flops_per_step(w)
+        res[name] = {"seq_len": L, "flops_per_step": fl, "params": workloads.param_count(w), "runs": []}
+        for mode, blocks in PLAN[name]:
+            if name == "cfg3":
+                model = AcousticSRU(w.proj, w.layers, w.logits, mode=mode)
+                run = lambda T: model.forward(X, T)
+            elif name == "cfg5":
+                if not pg:
+                    import socket
+                    import torch.distributed as dist
+                    s = socket.socket()
+                    s.bind(("127.0.0.1", 0))
+                    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                    os.environ.setdefault("MASTER_PORT", str(s.getsockname()[1]))
+                    s.close()
+                    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+                    pg = True
+                models = {}
+
+                def run(T, mode=mode):
+                    if T not in models:
+                        models[T] = partition.ShardedBidirSRU(
+                            w.layers, w.layers_bwd, 0, 1, partition.wide_sru_stage_factory(T, mode, 0))
+                    return models[T].forward(X)
+            else:
+                st = P.DeviceStack(w.kind, w.layers, mode=mode)
+                run = lambda T, st=st: st.forward(X, T)
+            for T in blocks:
+                ms = timed(lambda: run(T), a.reps, flush)
+                entry = {"mode": mode, "T_b": T, "ms": round(ms, 4), "steps_per_s": round(L / ms * 1e3, 1),
+                         "tflops": round(fl * L / ms / 1e9, 2)}
+                res[name]["runs"].append(entry)
+                print(name, entry, flush=True)
+            if name == "cfg3":
+                model.close()
+            elif name not in ("cfg5",):
+                st.close()
+        res[name]["wall_s"] = round(time.time() - t0, 1)
+        del X
+        torch.cuda.empty_cache()
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        json.dump(res, f, indent=1)
+    print("wrote", a.out)
+
+
+if __name__ == "__main__":
+    main()
