@@ -56,7 +56,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--configs", default="cfg1,cfg2,cfg3,cfg4,cfg5")
-    ap.add_argument("--out", default=os.path.join(REPO, "profiles", "configs_r1.json"))
+    ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
     a = ap.parse_args()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     res = {}
