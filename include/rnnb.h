@@ -131,7 +131,7 @@ rnnb_status rnnb_finalize(int kind, const void* out_gate, const void* C, const v
  * shared memory, 4 = grid size of `layer`, 5 = dynamic smem bytes,
  * 6 = 1 if the warp-specialised TMA kernel ran `layer`, 7 = pass width NT,
  * 8 = K-chunk staged per pipeline step, 9 = 1 if the tcgen05 tensor-core
- * kernel ran `layer`. */
+ * kernel ran `layer`, 10 = 1 if the register-resident FFMA kernel ran it. */
 rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value);
 
 #ifdef __cplusplus

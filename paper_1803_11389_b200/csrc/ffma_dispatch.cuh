@@ -3,7 +3,7 @@
 // instantiates the kernel for one (accumulate, weight) type pair.
 #pragma once
 #include <cstdlib>
-#include "ffma_ws.cuh"
+#include "ffma_reg.cuh"
 
 namespace rnnb {
 
@@ -33,6 +33,7 @@ struct FfmaPlan {
   int nt = 1;
   bool wsmem = false;
   bool ws = false;  // warp-specialised TMA/mbarrier kernel (ffma_ws.cuh)
+  bool reg = false; // register-resident weights kernel (ffma_reg.cuh)
   int kc = 0;
   size_t smem = 0;
 };
@@ -120,8 +121,47 @@ static FfmaPlan plan_nt(int Dp, bool allow_wsmem) {
   return p;
 }
 
+// Register-resident fp32 kernel (ffma_reg.cuh): U in {4, 7}, aligned 16-byte
+// x rows, K = taps*D small enough that the FMA warps + epilogue warp fit the
+// register file (U=7: 84 weight registers, <= 8 FMA warps -> K <= 1024; U=4:
+// 48 weight registers, <= 16 FMA warps -> K <= 2048).  Chosen for small T_b,
+// where the shared-memory kernel re-reads every weight from SMEM for only
+// T_b FMAs (RNNB_REG=0/1 overrides).
+template <typename TA, typename TW, int CELL, int U>
+static bool reg_eligible(const LayerArgs<TA, TW>& a) {
+  if constexpr (!(sizeof(TA) == 4 && sizeof(TW) == 4 && (U == 7 || U == 4))) {
+    return false;
+  } else {
+    const int taps = CELL == QRNN ? 2 : 1;
+    auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    const int kmax = U == 7 ? 1024 : 2048;
+    if (a.G != nullptr || a.xround != XR_NONE || (a.D % 4) != 0 || taps * a.Dp > kmax) return false;
+    if ((a.ldx % 4) != 0 || !al(a.X) || (a.xcarry != nullptr && !al(a.xcarry))) return false;
+    const char* env = getenv("RNNB_REG");
+    if (env) return env[0] == '1';
+    return a.T_b <= 2;  // measured crossover (cfg1: 2.77 M flat vs SMEM kernel 1.26 / 1.81 / 3.17 M at T_b 1/2/4)
+  }
+}
+
+template <int CELL, int U>
+static cudaError_t launch_reg(const LayerArgs<float, float>& a, int grid, cudaStream_t s) {
+  const int taps = CELL == QRNN ? 2 : 1;
+  const int nkv = taps * a.Dp / 4;
+  const int threads = (nkv + 31) / 32 * 32 + 32;
+  ffma_reg_kernel<CELL, U><<<grid, threads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename TA, typename TW, int CELL, int NT, int U>
 static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaStream_t s, FfmaPlan* out) {
+  if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4 && (U == 7 || U == 4)) {
+    if (reg_eligible<TA, TW, CELL, U>(a)) {
+      FfmaPlan p;
+      p.nt = 1; p.wsmem = false; p.ws = false; p.reg = true; p.kc = 0; p.smem = 0;
+      if (out) *out = p;
+      return launch_reg<CELL, U>(a, grid, s);
+    }
+  }
   if (allow_wsmem && ws_eligible(a)) {
     using WC = WsCfg<TA, TW, CELL, NT, U>;
     constexpr int BWMAX = 512 / (int)sizeof(TA);  // 512-byte TMA boxes

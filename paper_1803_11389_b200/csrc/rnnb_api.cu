@@ -665,6 +665,7 @@ rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value) {
     case 7: *value = h->layers[layer].last.nt; return RNNB_OK;
     case 8: *value = h->layers[layer].last.kc; return RNNB_OK;
     case 9: *value = h->layers[layer].last_tc ? 1 : 0; return RNNB_OK;
+    case 10: *value = h->layers[layer].last.reg ? 1 : 0; return RNNB_OK;
     default: return fail(RNNB_EINVAL, "unknown query");
   }
 }

@@ -435,3 +435,25 @@ def test_f32x3_split_tensor_core_meets_fp32_bound(P, oracle, kind):
     assert e3 <= 5e-5
     st.close()
     f32.close()
+
+
+@pytest.mark.parametrize("kind,d", [("sru", 1024), ("sru", 512), ("qrnn", 512), ("qrnn", 1024)])
+def test_register_resident_kernel(P, oracle, kind, d, monkeypatch):
+    """ffma_reg (weights in registers, FFMA2, epilogue warp) at small T_b vs
+    the oracle and vs the shared-memory kernel (U=7 for d=1024 SRU, U=4 for
+    d=512; QRNN d=1024 is K=2048 with U=7: not eligible, SMEM kernel runs)."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 2, 57, np.float32)
+    X = torch.from_numpy(np.random.default_rng(14).standard_normal((333, d)).astype(np.float32)).cuda()
+    st = P.DeviceStack(kind, layers)
+    for T in (1, 2, 3, 8):
+        monkeypatch.setenv("RNNB_REG", "1")
+        H = st.forward(X, T).cpu().numpy()
+        used = st.query(10)
+        assert used == (0 if (kind == "qrnn" and d == 1024) else 1)
+        monkeypatch.setenv("RNNB_REG", "0")
+        Hs = st.forward(X, T).cpu().numpy()
+        ref = oracle.run_blocked(kind, layers, X.cpu().numpy(), T)
+        assert_f32(H, ref)
+        assert_f32(Hs, ref)
+    st.close()

@@ -34,4 +34,4 @@ for T in [int(b) for b in a.blocks.split(",")]:
     ms = e0.elapsed_time(e1) / a.reps
     print(f"{a.workload} {a.mode} T_b={T:3d}: {ms:8.4f} ms  {L / ms * 1e3 / 1e6:7.3f} M steps/s  "
           f"{fl * L / ms / 1e9:7.2f} TFLOP/s  ws={st.query(6)} nt={st.query(7)} kc={st.query(8)} "
-          f"smem={st.query(5)} grid={st.query(4)}", flush=True)
+          f"smem={st.query(5)} grid={st.query(4)} reg={st.query(10)} tc={st.query(9)}", flush=True)
