@@ -126,7 +126,7 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
 bool use_tc(const rnnb_stack* h, int64_t Tb) {
   if (getenv("RNNB_NO_TC") != nullptr || Tb < 16) return false;
   if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) return Tb <= 128;
-  if (h->mode == RNNB_F32X3) return Tb <= 64;
+  if (h->mode == RNNB_F32X3) return Tb <= 32;
   return false;
 }
 

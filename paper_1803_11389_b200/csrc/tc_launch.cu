@@ -66,7 +66,7 @@ static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUten
   return cudaGetLastError();
 }
 
-int tc_max_n(int mode) { return mode == TC_3XTF32 ? 64 : 128; }
+int tc_max_n(int mode) { return mode == TC_3XTF32 ? 32 : 128; }
 
 int tc_pick_n(int T_b) {
   if (T_b <= 16) return 16;
@@ -81,9 +81,10 @@ static cudaError_t run_n(int N, const TcArgs& a, const CUtensorMap& tw, const CU
   switch (N) {
     case 16: return launch_tc<CELL, MODE, 16>(a, tw, tx, grid, s);
     case 32: return launch_tc<CELL, MODE, 32>(a, tw, tx, grid, s);
-    case 64: return launch_tc<CELL, MODE, 64>(a, tw, tx, grid, s);
     default:
-      if constexpr (MODE == TC_3XTF32) return cudaErrorInvalidValue;  // stages would not fit
+      // 3xTF32 keeps the 3N chunk partials in registers: N <= 32
+      if constexpr (MODE == TC_3XTF32) return cudaErrorInvalidValue;
+      else if (N == 64) return launch_tc<CELL, MODE, 64>(a, tw, tx, grid, s);
       else return launch_tc<CELL, MODE, 128>(a, tw, tx, grid, s);
   }
 }

@@ -169,6 +169,45 @@ __device__ __forceinline__ float ld_cg(const float* p) {
 // named barrier 2 over the four epilogue warps
 __device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
 
+// Publish block b's AGGREGATE carry map, run the deterministic fixed-depth
+// look-back (composes the aggregates of blocks b-1 .. b-kLB, in fixed order,
+// onto the INCLUSIVE carry of block b-kLB-1 or c_0 -- timing never changes
+// the arithmetic, so results are run-to-run and chunking/GPU-count
+// invariant), publish block b's INCLUSIVE carry and return c_in.  Called by
+// the 128 epilogue threads (et = 0..127, thread = unit of tile u).
+__device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int unit, int et, float Ablk,
+                                             float Bblk) {
+  const size_t sidx = (size_t)b * a.Hpad + unit;
+  a.aggA[sidx] = Ablk;
+  a.aggB[sidx] = Bblk;
+  __threadfence();
+  tc_epi_sync();
+  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 1);
+  const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
+  // lanes of the first epilogue warp wait for the statuses in parallel
+  if (et < 32) {
+    const int j = b - 1 - et;
+    if (j >= jlo) while (ld_acquire(&a.status[(size_t)j * a.nU + u]) < 1) __nanosleep(32);
+    const int jb = jlo - 1;  // block whose inclusive carry anchors the chain
+    if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < 2) __nanosleep(32);
+  }
+  tc_epi_sync();
+  float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
+  for (int j = b - 1; j >= jlo; --j) {
+    const size_t jidx = (size_t)j * a.Hpad + unit;
+    const float Aj = ld_cg(&a.aggA[jidx]), Bj = ld_cg(&a.aggB[jidx]);
+    Bacc = Aacc * Bj + Bacc;
+    Aacc = Aacc * Aj;
+  }
+  const float anchor = jlo > 0 ? ld_cg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit]) : ld_cg(&a.cbuf[unit]);
+  const float cin = Aacc * anchor + Bacc;
+  a.incl[sidx] = Ablk * cin + Bblk;
+  __threadfence();
+  tc_epi_sync();
+  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 2);
+  return cin;
+}
+
 template <int MODE, int N>
 struct TcCfg {
   static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
@@ -181,6 +220,13 @@ struct TcCfg {
                                                                           : 2;
   static constexpr int ACC_COLS = 3 * N;
   static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;
+  // 3xTF32: the tensor cores' fp32 accumulation error grows linearly with the
+  // reduction length (measured), so K is accumulated in CK-k-tile chunks
+  // (K = 128) in alternating TMEM buffers and the chunk partials are summed
+  // in fp32 registers by the epilogue (keeps 3xTF32 inside the fp32 bound)
+  static constexpr bool CHUNKED = MODE == TC_3XTF32;
+  static constexpr int CK = 4;
+  static_assert(!CHUNKED || (N <= 32 && NACC == 2), "chunked accumulation keeps 3N partials in registers");
   static constexpr int TMEM_COLS = (NACC * ACC_COLS <= 32) ? 32 : (NACC * ACC_COLS <= 64) ? 64
                                    : (NACC * ACC_COLS <= 128) ? 128 : (NACC * ACC_COLS <= 256) ? 256 : 512;
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
@@ -248,12 +294,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = tc_idesc<MODE>(128, N);
       uint32_t it = 0, acc_it = 0;
-      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
-        const int ab = acc_it % C::NACC;
-        mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t dbase = tmem + ab * C::ACC_COLS;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int ab = acc_it % C::NACC;
+        uint32_t dbase = tmem + ab * C::ACC_COLS;
+        if (!C::CHUNKED) {
+          mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
+          tc_fence_after();
+        }
         for (int kt = 0; kt < a.nK; ++kt, ++it) {
+          const int kc = C::CHUNKED ? kt % C::CK : kt;  // k-tile index inside the accumulation
+          if (C::CHUNKED && kc == 0) {  // a new K-chunk accumulates into a fresh buffer
+            ab = acc_it % C::NACC;
+            dbase = tmem + ab * C::ACC_COLS;
+            mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
+            tc_fence_after();
+          }
           const int s = it % C::STAGES;
           mbar_wait(&full[s], (it / C::STAGES) & 1);
           tc_fence_after();
@@ -270,7 +325,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               if (C::SPLIT == 2) {
                 const uint64_t blo = sw128_desc(st + HALF + 3 * C::A_BYTES) + koff;
                 const uint64_t alo = sw128_desc(st + HALF + g * C::A_BYTES) + koff;
-                tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kt | kk) != 0);
+                tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kc | kk) != 0);
                 tc_mma<MODE>(dbase + g * N, adesc0 + koff, blo, idesc, 1);
                 tc_mma<MODE>(dbase + g * N, alo, bdesc0 + koff, idesc, 1);
               } else {
@@ -279,8 +334,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
           tc_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+          if (C::CHUNKED && (kc == C::CK - 1 || kt == a.nK - 1)) {
+            tc_commit(&acc_full[ab]);  // this K-chunk's partial products complete
+            ++acc_it;
+          }
         }
-        tc_commit(&acc_full[ab]);  // accumulators of this item complete
+        if (!C::CHUNKED) {
+          tc_commit(&acc_full[ab]);  // accumulators of this item complete
+          ++acc_it;
+        }
       }
     }
   } else {
@@ -296,22 +358,78 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int row = q * 32 + lane;          // unit within the tile
     const int et = threadIdx.x - 64;        // 0..127
     uint32_t acc_it = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++acc_it) {
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
       const int64_t t0 = (int64_t)b * a.T_b;
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       const int unit = u * 128 + row;
-      const int ab = acc_it % C::NACC;
-      mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
-      tc_fence_after();
       float bf = 0.f, br = 0.f;
       if (CELL == SRU && a.bias) {
         bf = a.bias[(size_t)unit * 2];
         br = a.bias[(size_t)unit * 2 + 1];
       }
+      float Ablk = 1.f, Bblk = 0.f;
+      if constexpr (C::CHUNKED) {
+        // sum the K-chunk partials in fp32 registers, then all phases from registers
+        float rz[N], rf[N], ro[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) rz[j] = rf[j] = ro[j] = 0.f;
+        const int nch = (a.nK + C::CK - 1) / C::CK;
+        for (int ch = 0; ch < nch; ++ch, ++acc_it) {
+          const int ab = acc_it % C::NACC;
+          mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
+          tc_fence_after();
+          const uint32_t tb = tmem + ab * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+#pragma unroll
+          for (int c0 = 0; c0 < N; c0 += 16) {
+            float pz[16], pf[16], po[16];
+            tmem_ld16(tb + 0 * N + c0, pz);
+            tmem_ld16(tb + 1 * N + c0, pf);
+            tmem_ld16(tb + 2 * N + c0, po);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              rz[c0 + j] += pz[j];
+              rf[c0 + j] += pf[j];
+              ro[c0 + j] += po[j];
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(&acc_empty[ab]);
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          if (CELL == SRU) {
+            rf[j] = sigmoid_ref<float>(rf[j] + bf);
+            ro[j] = sigmoid_ref<float>(ro[j] + br);
+          } else {
+            rz[j] = tanh_full(rz[j]);
+            rf[j] = sigmoid_ref<float>(rf[j]);
+            ro[j] = sigmoid_ref<float>(ro[j]);
+          }
+          if (j < l) {
+            Bblk = rf[j] * Bblk + (1.f - rf[j]) * rz[j];
+            Ablk = rf[j] * Ablk;
+          }
+        }
+        const float cin = tc_lookback(a, b, u, unit, et, Ablk, Bblk);
+        float c = cin;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          if (j < l && unit < a.H) {
+            c = rf[j] * c + (1.f - rf[j]) * rz[j];
+            float h = ro[j] * tanh_full(c);
+            if (CELL == SRU) h = h + (1.f - ro[j]) * a.Xhw[(t0 + j) * a.ldhw + unit];
+            a.Hout[(t0 + j) * a.ldh + unit] = h;
+          }
+        }
+        if (b == a.nB - 1 && unit < a.Hpad) a.cbuf[unit] = c;  // c_T of the sequence
+        continue;
+      }
+      const int ab = acc_it % C::NACC;
+      mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
+      tc_fence_after();
       const uint32_t tb = tmem + ab * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
       // (A) activations + block aggregate
-      float Ablk = 1.f, Bblk = 0.f;
       for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
         float pz[16], pf[16], po[16];
         tmem_ld16(tb + 0 * N + c0, pz);
@@ -337,43 +455,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tmem_st16(tb + 2 * N + c0, po);
       }
       tmem_st_wait();
-      const size_t sidx = (size_t)b * a.Hpad + unit;
-      a.aggA[sidx] = Ablk;
-      a.aggB[sidx] = Bblk;
-      __threadfence();
-      tc_epi_sync();
-      if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 1);
-      // (B) deterministic fixed-depth look-back: c_in(b) composes the
-      // aggregates of the kLB blocks b-1 .. b-kLB (fixed order, newest first)
-      // onto the INCLUSIVE carry of block b-kLB-1 (or c_0).  The arithmetic
-      // never depends on timing, so results are run-to-run and
-      // chunking/GPU-count invariant; the inclusive chain advances kLB+1
-      // blocks per hop.
-      float cin;
-      {
-        const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
-        // lanes of the first epilogue warp wait for the statuses in parallel
-        if (et < 32) {
-          const int j = b - 1 - et;
-          if (j >= jlo) while (ld_acquire(&a.status[(size_t)j * a.nU + u]) < 1) __nanosleep(32);
-          const int jb = jlo - 1;  // block whose inclusive carry anchors the chain
-          if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < 2) __nanosleep(32);
-        }
-        tc_epi_sync();
-        float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
-        for (int j = b - 1; j >= jlo; --j) {
-          const size_t jidx = (size_t)j * a.Hpad + unit;
-          const float Aj = ld_cg(&a.aggA[jidx]), Bj = ld_cg(&a.aggB[jidx]);
-          Bacc = Aacc * Bj + Bacc;
-          Aacc = Aacc * Aj;
-        }
-        const float anchor = jlo > 0 ? ld_cg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit]) : ld_cg(&a.cbuf[unit]);
-        cin = Aacc * anchor + Bacc;
-      }
-      a.incl[sidx] = Ablk * cin + Bblk;
-      __threadfence();
-      tc_epi_sync();
-      if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 2);
+      const float cin = tc_lookback(a, b, u, unit, et, Ablk, Bblk);
       // (C) sequential recurrence from c_in and the output mix
       float c = cin;
       for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
@@ -401,6 +483,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // TMEM buffer can be refilled
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
+      ++acc_it;
       if (b == a.nB - 1 && unit < a.Hpad) a.cbuf[unit] = c;  // c_T of the sequence
     }
   }

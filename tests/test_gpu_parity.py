@@ -411,28 +411,27 @@ def test_tensor_core_look_back_is_deterministic(P, oracle):
 
 @pytest.mark.parametrize("kind", ["sru", "qrnn"])
 def test_f32x3_split_tensor_core_meets_fp32_bound(P, oracle, kind):
-    """3xTF32 split products on tcgen05 (mode "f32x3", 16 <= T_b <= 64): the
-    reference's max-abs bound (1e-4) and normwise <= 5e-5 (NOT the 1e-5 fp32
-    bound: tensor-core fp32 accumulation over K=2048 leaves ~1.5e-5, so the
-    exact-fp32 "f32" mode stays on FFMA); error vs an f64 oracle reported."""
+    """3xTF32 split products on tcgen05 (mode "f32x3", 16 <= T_b <= 32) with
+    128-deep K chunks summed in fp32 meet the fp32 bound (normwise 1e-5,
+    max-abs 1e-4); the error vs an f64 oracle is reported beside FFMA's."""
     import torch
     d = 512
     layers = oracle.generate_layers(kind, d, d, 2, 51, np.float32)
     X = np.random.default_rng(12).standard_normal((600, d)).astype(np.float32)
     st = P.DeviceStack(kind, layers, mode="f32x3")
     ref64 = oracle.run_blocked(kind, [[m.astype(np.float64) for m in l] for l in layers], X.astype(np.float64), 32)
-    for T in (16, 32, 48, 64):
+    for T in (16, 24, 32):
         H = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
         assert st.query(9) == 1
         ref = oracle.run_blocked(kind, layers, X, T)
         print(f"{kind} T_b={T}: 3xTF32 vs fp32 oracle normwise {normwise(H, ref):.2e}")
-        assert normwise(H, ref) <= 5e-5 and np.max(np.abs(H - ref)) <= 1e-4
+        assert_f32(H, ref)
     e3 = normwise(H, ref64)
     f32 = P.DeviceStack(kind, layers, mode="f32")
-    Hf = f32.forward(torch.from_numpy(X).cuda(), 64).cpu().numpy()
+    Hf = f32.forward(torch.from_numpy(X).cuda(), 32).cpu().numpy()
     ef = normwise(Hf, ref64)
     print(f"normwise error vs f64: 3xTF32 {e3:.2e}  FFMA fp32 {ef:.2e}")
-    assert e3 <= 5e-5
+    assert e3 <= 5e-6
     st.close()
     f32.close()
 

@@ -29,9 +29,9 @@ from paper_1803_11389_b200.acoustic import AcousticSRU  # noqa: E402
 PLAN = {
     "cfg1": [("f32", (1, 4, 16))],
     "cfg2": [("f32", (1, 2, 4, 8, 16, 32, 64)), ("bf16", (16, 32, 64)), ("tf32", (16, 32, 64)),
-             ("f32x3", (16, 32, 64))],
+             ("f32x3", (16, 32))],
     "cfg3": [("f32", (1, 8, 32)), ("bf16", (1, 8, 32)), ("tf32", (8, 32))],
-    "cfg4": [("bf16", (32,)), ("f32", (32,))],
+    "cfg4": [("bf16", (32,)), ("f32x3", (32,)), ("f32", (32,))],
     "cfg5": [("bf16", (16, 64))],
 }
 
