@@ -123,10 +123,17 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
   return a;
 }
 
+// Tensor-core path selection.  bf16/tf32: small T_b too (N = 16 with masked
+// columns below 16 -- one weight stream per block still beats the FFMA
+// kernel); f32x3: 16..32 (below 16 the exact FFMA kernel is faster).
 bool use_tc(const rnnb_stack* h, int64_t Tb) {
-  if (getenv("RNNB_NO_TC") != nullptr || Tb < 16) return false;
-  if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) return Tb <= 128;
-  if (h->mode == RNNB_F32X3) return Tb <= 32;
+  if (getenv("RNNB_NO_TC") != nullptr) return false;
+  const char* mn = getenv("RNNB_TC_MIN");
+  // measured on cfg2: bf16 TC beats the FFMA kernel from T_b = 1 (1.26 vs 0.86 M
+  // steps/s), tf32 from T_b = 2 (1.29 vs 0.95)
+  const int lo = mn ? atoi(mn) : (h->mode == RNNB_BF16 ? 1 : 2);
+  if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) return Tb >= lo && Tb <= 128;
+  if (h->mode == RNNB_F32X3) return Tb >= 16 && Tb <= 32;
   return false;
 }
 
