@@ -48,7 +48,7 @@ static cudaError_t launch_ws_xr(const LayerArgs<TA, TW>& a, const CUtensorMap& t
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  k<<<grid, kWsThreads, smem, s>>>(a, tm);
+  k<<<grid, WsCfg<TA, TW, CELL, NT, U>::THREADS, smem, s>>>(a, tm);
   return cudaGetLastError();
 }
 

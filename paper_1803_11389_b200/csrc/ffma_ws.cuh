@@ -21,10 +21,8 @@
 
 namespace rnnb {
 
-constexpr int kWsComputeWarps = 16;
 constexpr int kWsEpiWarps = 2;
 constexpr int kWsEpiThreads = kWsEpiWarps * 32;
-constexpr int kWsThreads = (kWsComputeWarps + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group
 
 // named barrier 1 over the epilogue warpgroup only
 __device__ __forceinline__ void epi_bar_sync() {
@@ -83,10 +81,25 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 // packed fp32x2 FMA (sm_100): d = a * b + c on (lo, hi) float pairs
+// Two spellings, same instruction: the compiler builtin lets ptxas coalesce
+// accumulators in place (no register-rotation moves) but costs registers;
+// the inline-asm form is kept for kernels that run at the 96-register cap.
 __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  const float2 r = __ffma2_rn(*reinterpret_cast<const float2*>(&a), *reinterpret_cast<const float2*>(&b),
+                              *reinterpret_cast<const float2*>(&c));
+  return *reinterpret_cast<const unsigned long long*>(&r);
+}
+__device__ __forceinline__ unsigned long long ffma2_asm(unsigned long long a, unsigned long long b,
+                                                        unsigned long long c) {
   unsigned long long d;
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
+}
+template <bool kBuiltin>
+__device__ __forceinline__ unsigned long long ffma2_sel(unsigned long long a, unsigned long long b,
+                                                        unsigned long long c) {
+  if constexpr (kBuiltin) return ffma2(a, b, c);
+  else return ffma2_asm(a, b, c);
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -97,24 +110,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// Consumer mapping: kWsComputeWarps = KG k-groups x RG row-groups.  A warp
-// owns RH = ceil(R/RG) rows over its k-group's share of K; inside the warp
-// LANES_T lanes split the NT columns (CT columns each) and LANES_K lanes
-// split K.  Two columns per lane whenever NT >= 2 keeps the weight LDS
-// amortised over 2*KV FMAs; the x LDS over RH*KV FMAs.
+// Consumer mapping: CW = KG k-groups x RG row-groups of consumer warps.  A
+// warp owns RH = ceil(R/RG) rows over its k-group's share of K; inside the
+// warp LANES_T lanes split the NT columns (CT columns each) and LANES_K lanes
+// split K.  A weight LDS feeds CT*KV FMAs and an x LDS RH*KV, so the wide
+// tile (CT = 4, fp32, NT >= 16) halves the LDS per FMA of the narrow one;
+// it needs ~2x the accumulator registers, so it runs 8 consumer warps
+// (KG = 4) with up to 168 registers each instead of 16 with 96.
 template <typename TA, typename TW, int CELL, int NT, int U>
 struct WsCfg {
   static constexpr int KV = 16 / (int)sizeof(TA);
   static constexpr int TAPS = CELL == QRNN ? 2 : 1;
   static constexpr int R = 3 * U;
-  static constexpr int KG = 8, RG = 2;
-  static_assert(KG * RG == kWsComputeWarps, "consumer warp split");
+  static constexpr int CTW = (sizeof(TA) == 4 && NT >= 16) ? 4 : 2;
+  static constexpr int KG = CTW == 4 ? 4 : 8, RG = 2;
+  static constexpr int CW = KG * RG;                       // consumer warps
+  static constexpr int THREADS = (CW + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group
   static constexpr int RH = (R + RG - 1) / RG;
   static constexpr int Rpad = RH * RG;
   // smem row count per k-vector: odd so consecutive kv (lanes kq) hit distinct
   // 16-byte bank groups; rows [R, Rpad) read garbage that is never used
   static constexpr int Rs = (R % 2) ? R : R + 1;
-  static constexpr int LANES_T = NT >= 2 ? NT / 2 : 1;
+  static constexpr int LANES_T = NT >= CTW ? NT / CTW : 1;
   static constexpr int CT = NT / LANES_T;
   static constexpr int LANES_K = 32 / LANES_T;
   static constexpr int KL = KG * LANES_K;
@@ -122,6 +139,9 @@ struct WsCfg {
   // must hit 8 distinct 16-byte bank groups; one row needs no padding
   static constexpr int PADV = LANES_T == 1 ? 0 : KV * (LANES_T >= 8 ? 1 : 8 / LANES_T);
   static constexpr int STAGES = 4;
+  // reduce-scatter over the LANES_K lanes of a k-group: NV partials per lane
+  // (padded to a multiple of LANES_K), NV / LANES_K sums per lane afterwards
+  static constexpr int NV = (RH * CT + LANES_K - 1) / LANES_K * LANES_K;
 };
 
 // x chunk of KC columns = KC/BW TMA boxes of [NT+1 rows x (BW + PADV) cols],
@@ -145,12 +165,13 @@ __host__ __device__ inline size_t ws_smem_bytes(int Dp, int KC, int BW) {
 }
 
 template <typename TA, typename TW, int CELL, int NT, int U, int XR>
-__global__ void __launch_bounds__(kWsThreads, 1)
+__global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
     ffma_ws_kernel(LayerArgs<TA, TW> a, const __grid_constant__ CUtensorMap tmx) {
   using C = WsCfg<TA, TW, CELL, NT, U>;
   constexpr int KV = C::KV, TAPS = C::TAPS, R = C::R, Rs = C::Rs, KG = C::KG, RH = C::RH, Rpad = C::Rpad;
   constexpr int LANES_T = C::LANES_T, CT = C::CT, LANES_K = C::LANES_K, KL = C::KL;
   constexpr int STAGES = C::STAGES;
+  constexpr int CW = C::CW, NTHR = C::THREADS;
   const int KC = a.KC;
   const int BW = a.KCB;                  // TMA box width (columns)
   const int BXS = BW + C::PADV;          // padded row pitch inside a box
@@ -186,7 +207,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   {
     constexpr int VB = KV * (int)sizeof(TW);  // bytes per (kv, r) vector
     const int nvec = R * Kv;
-    for (int i = tid; i < nvec; i += kWsThreads) {
+    for (int i = tid; i < nvec; i += NTHR) {
       const int r = i / Kv, kv = i - (i / Kv) * Kv;
       char* dst = reinterpret_cast<char*>(Ws) + ((size_t)kv * Rs + r) * VB;
       const char* src = reinterpret_cast<const char*>(Wg) + ((size_t)r * Kv + kv) * VB;
@@ -198,9 +219,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWsComputeWarps);
+      mbar_init(&empty[s], CW);
     }
-    mbar_init(redfull, kWsComputeWarps);
+    mbar_init(redfull, CW);
     mbar_init(redempty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -211,7 +232,7 @@ __global__ void __launch_bounds__(kWsThreads, 1)
   const int rot = (int)(blockIdx.x % (unsigned)nchunk);
   const int r0 = TAPS == 2 ? 0 : 1;  // SRU never reads row 0 (x_{t-1})
 
-  if (warp == kWsComputeWarps) {
+  if (warp == CW) {
     // ---------------- producer: TMA bulk copies of x-row chunks ----------------
     uint32_t seq = 0;
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
@@ -254,9 +275,9 @@ __global__ void __launch_bounds__(kWsThreads, 1)
         }
       }
     }
-  } else if (warp > kWsComputeWarps) {
+  } else if (warp > CW) {
     // ------------- epilogue warpgroup: sums, activations, scan, output -------------
-    const int et = tid - (kWsComputeWarps + 1) * 32;  // 0 .. kWsEpiThreads-1
+    const int et = tid - (CW + 1) * 32;  // 0 .. kWsEpiThreads-1
     TA c = TA(0);
     if (et < U && a.c_in != nullptr && u0 + et < a.H) c = a.c_in[u0 + et];
     uint32_t pass = 0;
@@ -312,6 +333,11 @@ __global__ void __launch_bounds__(kWsThreads, 1)
     const int rbase = rg * RH;
     // lane-constant x offset: box of k-vector kl, row tq+1 (tap 0, column tq)
     const int xlane = (kl >> LVPB) * BOXS + (tq + 1) * BXS + (kl & MVPB) * KV;
+    const TA* xlane_base = Xr + xlane;
+    const size_t stage_elems = stage_bytes / sizeof(TA);
+    const TW* wlane_base = Ws + ((size_t)kl * Rs + rbase) * KV;
+    const size_t w_chunk = (size_t)(KC / KV) * Rs * KV;  // weights of one chunk (all rows)
+    const int kv_last = (Dp - (nchunk - 1) * KC) / KV;    // k-vectors in the last chunk
     uint32_t seq = 0, pass = 0;
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
@@ -332,17 +358,22 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #pragma unroll
             for (int ct = 0; ct < (kPacked ? CT : 1); ++ct) acc2[r][ct] = 0ull;
         }
+        constexpr int kUnrollCh = 1;
+        // chunk index cc runs rot, rot+1, .. (mod nchunk) -- the producer's order;
+        // kept incrementally (no per-chunk division)
+        int cc = rot;
+#pragma unroll kUnrollCh
         for (int ch = 0; ch < nchunk; ++ch, ++seq) {
           const int s = seq % STAGES;
           if (!(a.dbg & 1)) mbar_wait(&full[s], (seq / STAGES) & 1);
-          const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
-          const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
-          const TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
+          const int ccur = cc;
+          cc = cc + 1 == nchunk ? 0 : cc + 1;
           // KC == KL*KV (host): every lane owns exactly one k-vector per tap per
-          // chunk, at a lane-constant offset inside the staged box
-          if (kl < kcs / KV) {
-            const TA* xl = xb + xlane;
-            const TW* wl = Ws + ((size_t)(d0 / KV + kl) * Rs + rbase) * KV;
+          // chunk, at a lane-constant offset inside the staged box; only the
+          // last chunk of a row can be partial
+          if (ccur != nchunk - 1 || kl < kv_last) {
+            const TA* xl = xlane_base + (size_t)s * stage_elems;
+            const TW* wl = wlane_base + (size_t)ccur * w_chunk;
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap) {
               const TW* wp = wl + (size_t)tap * (Dp / KV) * Rs * KV;
@@ -354,11 +385,12 @@ __global__ void __launch_bounds__(kWsThreads, 1)
 #pragma unroll
                 for (int r = 0; r < RH; ++r) {
                   const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(wp + r * KV);
+                  // both k-pair halves of a row: CT independent FFMA2 between
+                  // the two updates of one accumulator
 #pragma unroll
-                  for (int ct = 0; ct < CT; ++ct) {
-                    acc2[r][ct] = ffma2(w.x, xp[ct].x, acc2[r][ct]);
-                    acc2[r][ct] = ffma2(w.y, xp[ct].y, acc2[r][ct]);
-                  }
+                  for (int ct = 0; ct < CT; ++ct) acc2[r][ct] = ffma2_sel<C::CTW == 4>(w.x, xp[ct].x, acc2[r][ct]);
+#pragma unroll
+                  for (int ct = 0; ct < CT; ++ct) acc2[r][ct] = ffma2_sel<C::CTW == 4>(w.y, xp[ct].y, acc2[r][ct]);
                 }
               } else {
                 TA xv[CT][KV];
@@ -390,22 +422,35 @@ __global__ void __launch_bounds__(kWsThreads, 1)
             for (int ct = 0; ct < CT; ++ct)
               acc[r][ct] = __uint_as_float((unsigned)acc2[r][ct]) + __uint_as_float((unsigned)(acc2[r][ct] >> 32));
         }
+        // reduce-scatter over the LANES_K lanes of the k-group: at each level a
+        // lane keeps the half of its live partials selected by its lane bit
+        // and adds the partner's copy, so partial j ends in one lane only
+        constexpr int NV = C::NV;
+        TA v[NV];
 #pragma unroll
-        for (int r = 0; r < RH; ++r)
+        for (int j = 0; j < NV; ++j) v[j] = j < RH * CT ? acc[j / CT][j % CT] : TA(0);
 #pragma unroll
-          for (int ct = 0; ct < CT; ++ct) {
-            TA v = acc[r][ct];
+        for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) {
+          const bool upper = (lane & o) != 0;
 #pragma unroll
-            for (int o = LANES_T; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            acc[r][ct] = v;
+          for (int i = 0; i < ns; ++i) {
+            const TA send = upper ? v[i] : v[i + ns];
+            const TA keep = upper ? v[i + ns] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
           }
+        }
+        // lane bits (LANES_T, 2 LANES_T, ...) chose offsets (NV/2, NV/4, ...)
+        int jb = 0;
+#pragma unroll
+        for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) jb += (lane & o) ? ns : 0;
         mbar_wait(redempty, (pass & 1) ^ 1);
-        if (kq == 0) {
 #pragma unroll
-          for (int r = 0; r < RH; ++r)
-#pragma unroll
-            for (int ct = 0; ct < CT; ++ct)
-              red[((size_t)kg * Rpad + rbase + r) * NT + tq + LANES_T * ct] = acc[r][ct];
+        for (int i = 0; i < NV / LANES_K; ++i) {
+          const int j = jb + i;
+          if (j < RH * CT) {
+            const int r = j / CT, ct = j - (j / CT) * CT;
+            red[((size_t)kg * Rpad + rbase + r) * NT + tq + LANES_T * ct] = v[i];
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(redfull);
