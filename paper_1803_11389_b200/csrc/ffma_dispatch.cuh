@@ -152,6 +152,33 @@ static cudaError_t launch_reg(const LayerArgs<float, float>& a, int grid, cudaSt
   return cudaGetLastError();
 }
 
+// Warp-specialised kernel (ffma_ws.cuh) when its shared-memory plan fits.
+// Returns false (nothing launched) when the kernel cannot take this layer.
+template <typename TA, typename TW, int CELL, int NT, int U>
+static bool try_ws(LayerArgs<TA, TW> a, int grid, cudaStream_t s, FfmaPlan* out, cudaError_t* err) {
+  if (!ws_eligible(a)) return false;
+  using WC = WsCfg<TA, TW, CELL, NT, U>;
+  constexpr int BWMAX = 512 / (int)sizeof(TA);  // 512-byte TMA boxes
+  // one k-vector per consumer lane per tap per chunk (see ffma_ws.cuh)
+  int kc = WC::KL * WC::KV;
+  if (kc > a.Dp) kc = a.Dp;
+  int bw = WC::KV;  // power-of-two box width >= the chunk, capped at 512 bytes
+  while (bw < kc && bw < BWMAX) bw <<= 1;
+  const int nbox = (kc + bw - 1) / bw;
+  const size_t sm = ws_smem_bytes<TA, TW, CELL, NT, U>(a.Dp, nbox * bw, bw);
+  if (sm > kMaxSmem) return false;
+  CUtensorMap tm;
+  if (!make_x_map<TA>(&tm, a.X, a.D, a.L, a.ldx, bw + WC::PADV, NT + 1)) return false;
+  FfmaPlan p;
+  p.nt = NT; p.wsmem = true; p.ws = true; p.kc = kc; p.smem = sm;
+  a.KC = kc;
+  a.KCB = bw;
+  if (out) *out = p;
+  if constexpr (NT == 32) *err = launch_ws_xr<TA, TW, CELL, NT, U, XR_NONE>(a, tm, grid, sm, s);  // fp32 only
+  else *err = launch_ws<TA, TW, CELL, NT, U>(a, tm, grid, sm, s);
+  return true;
+}
+
 template <typename TA, typename TW, int CELL, int NT, int U>
 static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaStream_t s, FfmaPlan* out) {
   if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4 && (U == 7 || U == 4)) {
@@ -162,27 +189,9 @@ static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaS
       return launch_reg<CELL, U>(a, grid, s);
     }
   }
-  if (allow_wsmem && ws_eligible(a)) {
-    using WC = WsCfg<TA, TW, CELL, NT, U>;
-    constexpr int BWMAX = 512 / (int)sizeof(TA);  // 512-byte TMA boxes
-    do {
-      // one k-vector per consumer lane per tap per chunk (see ffma_ws.cuh)
-      int kc = WC::KL * WC::KV;
-      if (kc > a.Dp) kc = a.Dp;
-      int bw = WC::KV;  // power-of-two box width >= the chunk, capped at 512 bytes
-      while (bw < kc && bw < BWMAX) bw <<= 1;
-      const int nbox = (kc + bw - 1) / bw;
-      size_t sm = ws_smem_bytes<TA, TW, CELL, NT, U>(a.Dp, nbox * bw, bw);
-      if (sm > kMaxSmem) break;
-      CUtensorMap tm;
-      if (!make_x_map<TA>(&tm, a.X, a.D, a.L, a.ldx, bw + WC::PADV, NT + 1)) break;
-      FfmaPlan p;
-      p.nt = NT; p.wsmem = true; p.ws = true; p.kc = kc; p.smem = sm;
-      a.KC = kc;
-      a.KCB = bw;
-      if (out) *out = p;
-      return launch_ws<TA, TW, CELL, NT, U>(a, tm, grid, sm, s);
-    } while (0);
+  if (allow_wsmem) {
+    cudaError_t e;
+    if (try_ws<TA, TW, CELL, NT, U>(a, grid, s, out, &e)) return e;
   }
   FfmaPlan p = plan_nt<TA, TW, CELL, NT, U>(a.Dp, allow_wsmem);
   a.KC = p.kc;
@@ -198,7 +207,17 @@ static cudaError_t run_u(const LayerArgs<TA, TW>& a, int grid, bool allow_wsmem,
     case 2: return run_nt<TA, TW, CELL, 2, U>(a, grid, allow_wsmem, s, out);
     case 4: return run_nt<TA, TW, CELL, 4, U>(a, grid, allow_wsmem, s, out);
     case 8: return run_nt<TA, TW, CELL, 8, U>(a, grid, allow_wsmem, s, out);
-    default: return run_nt<TA, TW, CELL, 16, U>(a, grid, allow_wsmem, s, out);
+    default:
+      // fp32, opt-in (RNNB_NT32=1): a 32-column pass halves the per-pass
+      // reduction / hand-off cost but measured within +-3% of NT=16 (cfg2)
+      if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4) {
+        const char* env = getenv("RNNB_NT32");
+        if (allow_wsmem && a.T_b >= 32 && a.xround == XR_NONE && env && env[0] == '1') {
+          cudaError_t e;
+          if (try_ws<TA, TW, CELL, 32, U>(a, grid, s, out, &e)) return e;
+        }
+      }
+      return run_nt<TA, TW, CELL, 16, U>(a, grid, allow_wsmem, s, out);
   }
 }
 

@@ -456,3 +456,21 @@ def test_register_resident_kernel(P, oracle, kind, d, monkeypatch):
         assert_f32(H, ref)
         assert_f32(Hs, ref)
     st.close()
+
+
+@pytest.mark.parametrize("kind,d", [("sru", 1024), ("qrnn", 1024), ("qrnn", 520)])
+def test_wide_pass_kernels(P, oracle, kind, d, monkeypatch):
+    """ffma_ws wide tile (8 consumer warps, 11x4 FFMA2 tile, reduce-scatter)
+    at NT=16 and the opt-in NT=32 pass, including a remainder block and a
+    partial last K chunk (d=520), vs the oracle."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 2, 61, np.float32)
+    X = np.random.default_rng(15).standard_normal((301, d)).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    st = P.DeviceStack(kind, layers)
+    for nt32 in ("0", "1"):
+        monkeypatch.setenv("RNNB_NT32", nt32)
+        for T in (16, 32, 40, 64):
+            H = st.forward(Xd, T).cpu().numpy()
+            assert_f32(H, oracle.run_blocked(kind, layers, X, T))
+    st.close()

@@ -85,11 +85,94 @@ void run(const char* name, int sms, float* out) {
          cudaGetErrorString(cudaGetLastError()));
 }
 
+
+// scalar FFMA variant: acc[r][c] += w[r][e] * x[c][e] over the 4 k of a vector
+template <int R, int C, int LT, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_tile_s(float* out, int iters) {
+  constexpr int KVS = 64;
+  constexpr int LK = 32 / LT;
+  extern __shared__ __align__(16) float sm[];
+  constexpr int RS = R | 1;
+  float4* ws = reinterpret_cast<float4*>(sm);
+  float4* xs = ws + KVS * RS;
+  for (int i = threadIdx.x; i < KVS * RS + C * LT * (KVS + 1); i += blockDim.x)
+    ws[i] = make_float4(1e-3f * (i & 7), 2e-3f, 3e-3f, 4e-3f);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int tq = lane % LT, kq = lane / LT;
+  float acc[R][C];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[r][c] = 0.f;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll 2
+    for (int kb = 0; kb < KVS; kb += LK) {
+      const int kv = kb + kq;
+      float4 xv[C];
+#pragma unroll
+      for (int c = 0; c < C; ++c) xv[c] = xs[(tq + LT * c) * (KVS + 1) + kv];
+      const float4* wp = ws + kv * RS;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const float4 w = wp[r];
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[r][c] = fmaf(w.x, xv[c].x, acc[r][c]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[r][c] = fmaf(w.y, xv[c].y, acc[r][c]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[r][c] = fmaf(w.z, xv[c].z, acc[r][c]);
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc[r][c] = fmaf(w.w, xv[c].w, acc[r][c]);
+      }
+    }
+  }
+  float t = 0;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int c = 0; c < C; ++c) t += acc[r][c];
+  if (t == 12345.f) out[threadIdx.x] = t;
+}
+
+template <int R, int C, int LT, int THREADS>
+void run_s(const char* name, int sms, float* out) {
+  constexpr int KVS = 64;
+  const size_t smem = (size_t)(KVS * (R | 1) + C * LT * (KVS + 1)) * 16;
+  cudaFuncSetAttribute(k_tile_s<R, C, LT, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int iters = 400;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  k_tile_s<R, C, LT, THREADS><<<sms, THREADS, smem>>>(out, iters);
+  cudaEventRecord(a);
+  for (int i = 0; i < 5; ++i) k_tile_s<R, C, LT, THREADS><<<sms, THREADS, smem>>>(out, iters);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  ms /= 5;
+  const double fma_sm = (double)iters * (KVS / (32 / LT)) * 32 * R * C * 4 * (THREADS / 32);
+  printf("{\"tile\": \"scalar %s\", \"R\": %d, \"C\": %d, \"LT\": %d, \"threads\": %d, \"ms\": %.4f, \"fma_per_clk_sm\": %.1f, "
+         "\"tflops\": %.2f, \"err\": \"%s\"}\n",
+         name, R, C, LT, THREADS, ms, fma_sm / (ms * 1e-3) / 1.965e9, 2 * fma_sm * sms / (ms * 1e-3) / 1e12,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float* out;
   cudaMalloc(&out, 4096 * sizeof(float));
+  run_s<11, 4, 4, 256>("11x4", sms, out);
+  run_s<11, 4, 4, 384>("11x4", sms, out);
+  run_s<11, 4, 4, 512>("11x4", sms, out);
+  run_s<11, 8, 4, 256>("11x8", sms, out);
+  run_s<11, 8, 4, 384>("11x8", sms, out);
+  run_s<8, 8, 4, 384>("8x8", sms, out);
+  run_s<8, 8, 4, 512>("8x8", sms, out);
+  run_s<7, 8, 4, 512>("7x8", sms, out);
+  run_s<11, 2, 8, 512>("11x2", sms, out);
   run<11, 2, 8, 512>("11x2 (v2)", sms, out);
   run<11, 2, 8, 384>("11x2", sms, out);
   run<7, 4, 4, 384>("7x4", sms, out);
