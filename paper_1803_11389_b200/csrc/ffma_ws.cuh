@@ -21,6 +21,9 @@
 
 namespace rnnb {
 
+#ifndef RNNB_WIDE_MIN_NT
+#define RNNB_WIDE_MIN_NT 1
+#endif
 constexpr int kWsEpiWarps = 2;
 constexpr int kWsEpiThreads = kWsEpiWarps * 32;
 
@@ -122,7 +125,7 @@ struct WsCfg {
   static constexpr int KV = 16 / (int)sizeof(TA);
   static constexpr int TAPS = CELL == QRNN ? 2 : 1;
   static constexpr int R = 3 * U;
-  static constexpr int CTW = (sizeof(TA) == 4 && NT >= 16) ? 4 : 2;
+  static constexpr int CTW = (sizeof(TA) == 4 && NT >= RNNB_WIDE_MIN_NT) ? 4 : 2;
   static constexpr int KG = CTW == 4 ? 4 : 8, RG = 2;
   static constexpr int CW = KG * RG;                       // consumer warps
   static constexpr int THREADS = (CW + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group

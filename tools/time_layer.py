@@ -19,7 +19,9 @@ ap.add_argument("--scale", type=float, default=1.0)
 a = ap.parse_args()
 w = workloads.make(a.workload, scale=a.scale)
 st = P.DeviceStack(w.kind, w.layers, mode=a.mode)
-X = torch.from_numpy(w.X.astype(st.np_dtype)).cuda()
+Xn = w.X if w.X.shape[1] == st.d_in[0] else \
+    __import__("numpy").random.default_rng(0).standard_normal((w.seq_len, st.d_in[0])).astype("float32")
+X = torch.from_numpy(Xn.astype(st.np_dtype)).cuda()
 L = w.seq_len
 fl = workloads.flops_per_step(w)
 for T in [int(b) for b in a.blocks.split(",")]:
