@@ -183,6 +183,9 @@ template <typename TA, typename TW, int CELL, int NT, int U>
 static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaStream_t s, FfmaPlan* out) {
   if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4 && (U == 7 || U == 4)) {
     if (reg_eligible<TA, TW, CELL, U>(a)) {
+      // streaming input needs the ws kernel; refuse rather than change kernels
+      // (the caller falls back, so results stay identical to rnnb_forward)
+      if (a.x_ready != nullptr) return cudaErrorNotSupported;
       FfmaPlan p;
       p.nt = 1; p.wsmem = false; p.ws = false; p.reg = true; p.kc = 0; p.smem = 0;
       if (out) *out = p;
@@ -193,6 +196,7 @@ static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaS
     cudaError_t e;
     if (try_ws<TA, TW, CELL, NT, U>(a, grid, s, out, &e)) return e;
   }
+  if (a.x_ready != nullptr) return cudaErrorNotSupported;  // streaming needs the ws kernel; nothing launched
   FfmaPlan p = plan_nt<TA, TW, CELL, NT, U>(a.Dp, allow_wsmem);
   a.KC = p.kc;
   if (out) *out = p;

@@ -51,6 +51,12 @@ struct LayerArgs {
   int KCB;             // TMA box width inside a chunk (ws kernel)
   int xround;          // XRound
   int dbg;             // debug switches (RNNB_DEBUG): bit0 consumers skip the x-ready wait
+  // streaming (ws kernel only; rnnb_forward_host): rows of X present in
+  // device memory so far (written by the copy stream), and per-chunk counts
+  // of CTAs whose h rows of that chunk are stored (read by the copy-out stream)
+  const int* x_ready;
+  int* h_done;
+  int h_chunk;
 };
 
 constexpr int kThreads = 256;

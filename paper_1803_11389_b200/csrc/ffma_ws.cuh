@@ -104,6 +104,22 @@ __device__ __forceinline__ unsigned long long ffma2_sel(unsigned long long a, un
   if constexpr (kBuiltin) return ffma2(a, b, c);
   else return ffma2_asm(a, b, c);
 }
+// streaming input: spin (with back-off) until `need` rows of X are in device
+// memory, then order the following TMA (async-proxy) reads after that
+__device__ __forceinline__ void wait_rows(const int* ready, int need) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t ns = 64;
+    while (true) {
+      int v;
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
+      if (v >= need) break;
+      __nanosleep(ns);
+      ns = ns < 2048 ? ns * 2 : 2048;
+    }
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+  }
+  __syncwarp();
+}
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -248,6 +264,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           const uint32_t ph = (seq / STAGES) & 1;
           if (a.dbg & 1) continue;
           mbar_wait_sleep(&empty[s], ph ^ 1);
+          if (a.x_ready != nullptr && ch == 0) wait_rows(a.x_ready, (int)((tp + NT) < a.L ? (tp + NT) : a.L));
           const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
           const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
           TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
@@ -325,6 +342,10 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           }
         }
         epi_bar_sync();
+        if (a.h_done != nullptr && et == 0 && ((tp + nt) % a.h_chunk == 0 || tp + nt == a.L)) {
+          __threadfence();  // this CTA's h rows of the chunk (ordered by the barrier) before the count
+          atomicAdd(&a.h_done[(tp + nt - 1) / a.h_chunk], 1);
+        }
       }
     }
     if (et < U && a.c_out != nullptr && u0 + et < a.H) a.c_out[u0 + et] = c;

@@ -28,6 +28,12 @@ rnnb_status cuda_fail(cudaError_t e, const char* where) {
     if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
   } while (0)
 
+#define CU_TRY(expr)                                                                      \
+  do {                                                                                    \
+    CUresult _r = (expr);                                                                 \
+    if (_r != CUDA_SUCCESS) return fail(RNNB_ECUDA, "stream memory operation failed: " #expr); \
+  } while (0)
+
 struct Layer {
   int64_t din = 0, dh = 0;
   int Dp = 0;        // d_in padded to a multiple of 8
@@ -64,9 +70,47 @@ struct rnnb_stack {
   void* hostX = nullptr;  // e2e device staging
   void* hostH = nullptr;
   size_t hx_bytes = 0, hh_bytes = 0;
+  // rnnb_forward_host pipeline: copy-in / copy-out streams and per-chunk events
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev[2 * 8 + 2] = {};
+  // streaming forward_host (single-layer fp32 stacks): counters the copy
+  // streams and the layer kernel hand rows through
+  int* stream_ctr = nullptr;  // [0] rows of X resident, [1..] per-chunk CTA counts
+  const int* stream_ready = nullptr;
+  int* stream_done = nullptr;
+  int stream_chunk = 0;
+  bool stream_refused = false;
 };
 
 namespace {
+
+constexpr int64_t kMaxStreamChunks = 64;
+
+// Stream memory operations (driver API, fetched through the runtime so the
+// library does not link libcuda): write a 32-bit value / wait for one.
+typedef CUresult (*StreamWriteValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*StreamWaitValue32Fn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct StreamOps {
+  StreamWriteValue32Fn write = nullptr;
+  StreamWaitValue32Fn wait = nullptr;
+};
+StreamOps stream_ops() {
+  static StreamOps ops;
+  static bool done = false;
+  if (!done) {
+    done = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      ops.write = reinterpret_cast<StreamWriteValue32Fn>(p);
+    p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      ops.wait = reinterpret_cast<StreamWaitValue32Fn>(p);
+  }
+  return ops;
+}
 
 size_t elem_size(int mode) { return mode == RNNB_F64 ? 8 : 4; }
 size_t wsize(int mode) { return mode == RNNB_F64 ? 8 : (mode == RNNB_BF16 ? 2 : 4); }
@@ -120,6 +164,9 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
   a.H = (int)ly.dh;
   a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
   a.xround = h->mode == RNNB_BF16 ? XR_BF16 : (h->mode == RNNB_TF32 ? XR_TF32 : XR_NONE);
+  a.x_ready = h->stream_ready;
+  a.h_done = h->stream_done;
+  a.h_chunk = h->stream_chunk;
   return a;
 }
 
@@ -237,6 +284,10 @@ rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_
   a.T_b = (int)(Tb > (int64_t)1 << 30 ? (int64_t)1 << 30 : Tb);
   FfmaPlan plan;
   cudaError_t e = ffma_layer_run<TA, TW>(h->kind, ly.U, a, true, s, &plan);
+  if (e == cudaErrorNotSupported && a.x_ready != nullptr) {
+    h->stream_refused = true;  // streaming needs the ws kernel; nothing was launched
+    return fail(RNNB_EINVAL, "streaming input not supported for this layer");
+  }
   if (e != cudaSuccess) return cuda_fail(e, "ffma_layer launch");
   ly.last = plan;
   ly.grid = (int)((ly.dh + ly.U - 1) / ly.U);
@@ -388,6 +439,11 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
     if (p) cudaFree(p);
   if (h->hostX) cudaFree(h->hostX);
   if (h->hostH) cudaFree(h->hostH);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  if (h->stream_ctr) cudaFree(h->stream_ctr);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
   cudaSetDevice(cur);
   delete h;
   return RNNB_OK;
@@ -569,16 +625,115 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
   char* dX = static_cast<char*>(h->hostX);
   char* dC = dX + xb;
   char* dXC = dC + csz * es;
-  CUDA_TRY(cudaMemcpyAsync(dX, X, xb, cudaMemcpyHostToDevice, s));
+  if (!h->s_in) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    for (auto& e : h->ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const char* hX = static_cast<const char*>(X);
+  char* hH = static_cast<char*>(H);
+  char* dH = static_cast<char*>(h->hostH);
+  const int64_t T = block_size < 1 ? 1 : block_size;
   if (c_state) CUDA_TRY(cudaMemcpyAsync(dC, c_state, csz * es, cudaMemcpyHostToDevice, s));
+  else CUDA_TRY(cudaMemsetAsync(dC, 0, csz * es, s));
   if (x_carry) CUDA_TRY(cudaMemcpyAsync(dXC, x_carry, xsz * es, cudaMemcpyHostToDevice, s));
-  st = rnnb_forward(h, dX, din, L, block_size, h->hostH, dh, c_state ? dC : nullptr, x_carry ? dXC : nullptr, stream);
+  else CUDA_TRY(cudaMemsetAsync(dXC, 0, xsz * es, s));
+  cudaEvent_t ev_start = h->ev[16], ev_done = h->ev[17];
+
+  // Streaming (single-layer fp32 stacks, warp-specialised kernel): ONE layer
+  // launch consumes X while it is still being copied in -- its TMA producer
+  // waits on a device counter of resident rows that the copy-in stream bumps
+  // after each chunk (stream write-value) -- and each CTA counts the chunks
+  // whose h rows it has stored, so the copy-out stream (stream wait-value)
+  // drains chunk i while later chunks compute.
+  const char* env_s = getenv("RNNB_HOST_STREAM");
+  const bool want_stream = !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
+  StreamOps so = stream_ops();
+  if (want_stream && so.write && so.wait) {
+    // chunk: whole blocks, >= 128 steps, at most kMaxStreamChunks of them
+    int64_t sc = (L + kMaxStreamChunks - 1) / kMaxStreamChunks;
+    if (sc < 128) sc = 128;
+    sc = (sc + T - 1) / T * T;
+    const int64_t nsc = (L + sc - 1) / sc;
+    if (nsc <= kMaxStreamChunks) {
+      if (!h->stream_ctr) CUDA_TRY(cudaMalloc(&h->stream_ctr, (1 + kMaxStreamChunks) * sizeof(int)));
+      CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (1 + nsc) * sizeof(int), s));
+      CUDA_TRY(cudaEventRecord(ev_start, s));
+      CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
+      CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
+      h->stream_ready = h->stream_ctr;
+      h->stream_done = h->stream_ctr + 1;
+      h->stream_chunk = (int)sc;
+      h->stream_refused = false;
+      st = rnnb_forward(h, dX, din, L, block_size, dH, dh, dC, dXC, stream);
+      h->stream_ready = nullptr;
+      h->stream_done = nullptr;
+      if (st == RNNB_OK) {
+        const unsigned grid = (unsigned)h->layers[0].grid;
+        for (int64_t i = 0; i < nsc; ++i) {
+          const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
+          CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice,
+                                   h->s_in));
+          CU_TRY(so.write(h->s_in, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
+        }
+        for (int64_t i = 0; i < nsc; ++i) {
+          const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
+          CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 1 + i), grid, CU_STREAM_WAIT_VALUE_GEQ));
+          CUDA_TRY(cudaMemcpyAsync(hH + t0 * dh * es, dH + t0 * dh * es, n * dh * es, cudaMemcpyDeviceToHost,
+                                   h->s_out));
+        }
+        CUDA_TRY(cudaEventRecord(ev_done, h->s_out));
+        CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
+        if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
+        if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        if (cur != h->device) cudaSetDevice(cur);
+        return st;
+      }
+      if (!h->stream_refused) {
+        if (cur != h->device) cudaSetDevice(cur);
+        return st;
+      }
+      st = RNNB_OK;  // the layer cannot stream: chunked pipeline below
+    }
+  }
+
+  // Time is cut into chunks of whole blocks; chunk i's copy-in (s_in), its
+  // forward (s, state carried in dC / dXC exactly as across blocks) and its
+  // copy-out (s_out) overlap the neighbouring chunks' copies.  Chunking at
+  // block boundaries leaves every value bitwise unchanged.
+  const char* env = getenv("RNNB_HOST_CHUNK");
+  const int64_t want = env ? atoll(env) : 512;  // steps per chunk
+  int64_t nch = want > 0 ? (L + want - 1) / want : 1;
+  if (nch > 8) nch = 8;
+  if (nch < 1) nch = 1;
+  int64_t cl = ((L + nch - 1) / nch + T - 1) / T * T;
+  nch = (L + cl - 1) / cl;
+  CUDA_TRY(cudaEventRecord(ev_start, s));  // staging buffers are free once earlier work on s is done
+  CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
+  CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
+  int64_t launches = 0;
+  for (int64_t i = 0; i < nch && st == RNNB_OK; ++i) {
+    const int64_t t0 = i * cl, n = (L - t0) < cl ? (L - t0) : cl;
+    cudaEvent_t ein = h->ev[2 * i], eout = h->ev[2 * i + 1];
+    CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice, h->s_in));
+    CUDA_TRY(cudaEventRecord(ein, h->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(s, ein, 0));
+    st = rnnb_forward(h, dX + t0 * din * es, din, n, block_size, dH + t0 * dh * es, dh, dC, dXC, stream);
+    launches += h->last_launches;
+    if (st != RNNB_OK) break;
+    CUDA_TRY(cudaEventRecord(eout, s));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_out, eout, 0));
+    CUDA_TRY(cudaMemcpyAsync(hH + t0 * dh * es, dH + t0 * dh * es, n * dh * es, cudaMemcpyDeviceToHost, h->s_out));
+  }
+  h->last_launches = launches;
+  CUDA_TRY(cudaEventRecord(ev_done, h->s_out));
+  CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
   if (st == RNNB_OK) {
-    CUDA_TRY(cudaMemcpyAsync(H, h->hostH, hb, cudaMemcpyDeviceToHost, s));
     if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
     if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
   }
+  CUDA_TRY(cudaStreamSynchronize(s));
   if (cur != h->device) cudaSetDevice(cur);
   return st;
 }

@@ -474,3 +474,33 @@ def test_wide_pass_kernels(P, oracle, kind, d, monkeypatch):
             H = st.forward(Xd, T).cpu().numpy()
             assert_f32(H, oracle.run_blocked(kind, layers, X, T))
     st.close()
+
+
+@pytest.mark.parametrize("kind,d,L,T", [("qrnn", 1024, 2048, 32), ("qrnn", 1024, 1000, 16), ("sru", 1024, 777, 8),
+                                        ("qrnn", 512, 300, 1), ("sru", 256, 130, 200), ("qrnn", 1024, 9000, 32)])
+def test_host_streaming_matches_device(P, oracle, kind, d, L, T, monkeypatch):
+    """rnnb_forward_host's streaming mode (one layer launch fed by the copy
+    stream through a device row counter, chunks drained by a wait-value copy
+    stream) and its chunked fallback are bitwise equal to the device call,
+    including carried c / x_carry in-out state."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 1, 71, np.float32)
+    X = np.random.default_rng(16).standard_normal((L, d)).astype(np.float32)
+    st = P.DeviceStack(kind, layers)
+    c0 = np.random.default_rng(17).standard_normal(d).astype(np.float32)
+    x0 = np.random.default_rng(18).standard_normal(d).astype(np.float32)
+    cd, xd = torch.from_numpy(c0.copy()).cuda(), torch.from_numpy(x0.copy()).cuda()
+    ref = st.forward(torch.from_numpy(X).cuda(), T, c_state=cd, x_carry=xd if kind == "qrnn" else None)
+    ref = ref.cpu().numpy()
+    for mode in ("1", "0"):
+        monkeypatch.setenv("RNNB_HOST_STREAM", mode)
+        c, x = c0.copy(), x0.copy()
+        H = st.forward_host(X, T, c_state=c, x_carry=x if kind == "qrnn" else None)
+        assert H.tobytes() == ref.tobytes(), mode
+        assert c.tobytes() == cd.cpu().numpy().tobytes()
+        if kind == "qrnn":
+            assert x.tobytes() == xd.cpu().numpy().tobytes()
+        H2 = st.forward_host(X, T)  # zero state, twice (counter / event reuse)
+        H3 = st.forward_host(X, T)
+        assert H2.tobytes() == H3.tobytes()
+    st.close()
