@@ -114,8 +114,13 @@ class ClockSampler:
 # our arm
 
 
-def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
-    """Dominant kernel = the fused layer kernel (one launch per layer)."""
+def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc=None):
+    """Dominant kernel = the fused layer kernel (one launch per layer).  The
+    pipe follows the kernel that actually ran (`tc`: the tcgen05 kernel ran
+    every layer); tensor-core modes that fell back to the FFMA kernel are
+    rated against the CUDA-core peak."""
+    if tc is None:
+        tc = mode in ("bf16", "tf32", "f32x3")
     L = w.seq_len
     flops = workloads.flops_per_step(w) * L / launches_per_step
     s_w = {"f32": 4, "tf32": 4, "bf16": 2, "f64": 8, "f32x3": 8}[mode]
@@ -126,7 +131,7 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
     bytes_model = (params * s_w * nblocks + (w.X.shape[1] + w.layers[-1].d_h) * s_a * L) / launches_per_step
     sec = ms_per_launch / 1e3
     mhz = pk.get("sm_max_mhz", 1965.0)
-    if mode in ("f32", "f64"):
+    if not tc:
         # CUDA-core pipe: MEASURED_PEAKS.json has no CUDA-core figure, so use the
         # FFMA throughput measured on this pool by tools/ffma_peak.cu
         fp = os.path.join(REPO, "profiles", "ffma_peak.json")
@@ -150,7 +155,7 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic):
     achieved = flops / sec / 1e12
     hbm = pk["hbm_gbs"]
     return {
-        "bound": "tensor" if mode in ("bf16", "tf32", "f32x3") else "compute",
+        "bound": "tensor" if tc else "compute",
         "pipe": pipe,
         "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
         "frac": round(achieved / peak, 4), "peak_source": src,
@@ -190,6 +195,7 @@ def time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_
         launches = st.last_launches
         tc = [bool(st.query(9, li)) for li in range(st.n_layers)]
         ws = [bool(st.query(6, li)) for li in range(st.n_layers)]
+        rg = [bool(st.query(10, li)) for li in range(st.n_layers)]
         ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         if dist:
             torch.distributed.barrier()
@@ -214,11 +220,13 @@ def time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             ms_step = float(t.item())
         results[T_b] = {"ms_per_step": ms_step, "ms_min": min(ms), "launches": launches, "clocks": clocks,
-                        "tcgen05": tc, "ffma_ws": ws}
+                        "tcgen05": tc, "ffma_ws": ws, "ffma_reg": rg}
     return results
 
 
 def kernel_name(r):
+    if all(r.get("ffma_reg", [False])):
+        return "ffma_reg (weights in registers, FFMA2, epilogue warp)"
     if all(r["tcgen05"]):
         return "tc_layer (tcgen05 + TMEM + TMA, look-back carry)"
     if all(r["ffma_ws"]):
@@ -290,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
         out_ = {}
         for T_b, r in res.items():
             rf = roofline_for(w, T_b, mode, r["ms_per_step"] / (r["launches"] or 1), r["launches"] or 1,
-                              pk, None)
+                              pk, None, tc=all(r["tcgen05"]))
             out_[str(T_b)] = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
                               "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"],
                               "tflops": rf["achieved"], "pipe": rf["pipe"], "kernel": kernel_name(r),
@@ -299,7 +307,8 @@ def run_ours(args, rank, world, local_rank):
 
     head = results[args.block]
     roof = roofline_for(w, args.block, args.mode, head["ms_per_step"] / (head["launches"] or 1),
-                        head["launches"] or 1, pk, load_traffic(args.workload, args.block, args.mode))
+                        head["launches"] or 1, pk, load_traffic(args.workload, args.block, args.mode),
+                        tc=all(head["tcgen05"]))
     roof["peaks_file"] = pk_src
     resident = [bool(st.query(3, li)) for li in range(st.n_layers)]
     line = {

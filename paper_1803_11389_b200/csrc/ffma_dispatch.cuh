@@ -48,6 +48,21 @@ static cudaError_t launch_ws_xr(const LayerArgs<TA, TW>& a, const CUtensorMap& t
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
+  if constexpr (XR == XR_NONE && sizeof(TA) == 4 && sizeof(TW) == 4) {
+    if (a.x_ready != nullptr) {
+      auto ks = ffma_ws_kernel<TA, TW, CELL, NT, U, XR, true>;
+      static bool attr_s = false;
+      if (!attr_s) {
+        cudaError_t e = cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+        if (e != cudaSuccess) return e;
+        attr_s = true;
+      }
+      ks<<<grid, WsCfg<TA, TW, CELL, NT, U>::THREADS, smem, s>>>(a, tm);
+      return cudaGetLastError();
+    }
+  } else {
+    if (a.x_ready != nullptr) return cudaErrorNotSupported;
+  }
   k<<<grid, WsCfg<TA, TW, CELL, NT, U>::THREADS, smem, s>>>(a, tm);
   return cudaGetLastError();
 }

@@ -57,6 +57,7 @@ struct LayerArgs {
   const int* x_ready;
   int* h_done;
   int h_chunk;
+  int* stream_fail;    // set by the kernel if streamed rows did not arrive in time
 };
 
 constexpr int kThreads = 256;

@@ -105,20 +105,34 @@ __device__ __forceinline__ unsigned long long ffma2_sel(unsigned long long a, un
   else return ffma2_asm(a, b, c);
 }
 // streaming input: spin (with back-off) until `need` rows of X are in device
-// memory, then order the following TMA (async-proxy) reads after that
-__device__ __forceinline__ void wait_rows(const int* ready, int need) {
+// memory, then order the following TMA (async-proxy) reads after that.  If
+// the rows do not arrive within kStreamTimeoutNs of kernel start (e.g. a
+// profiler serialises the copy stream behind this kernel) the kernel stops
+// waiting, flags *fail and runs to completion on whatever is there -- the
+// host sees the flag and recomputes without streaming.  Returns false on
+// time-out.
+constexpr uint64_t kStreamTimeoutNs = 2000000000ull;
+__device__ __forceinline__ bool wait_rows(const int* ready, int need, uint64_t t_start, int* fail) {
+  int ok = 1;
   if ((threadIdx.x & 31) == 0) {
     uint32_t ns = 64;
     while (true) {
       int v;
       asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
       if (v >= need) break;
+      uint64_t now;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t_start > kStreamTimeoutNs) {
+        atomicExch(fail, 1);
+        ok = 0;
+        break;
+      }
       __nanosleep(ns);
       ns = ns < 2048 ? ns * 2 : 2048;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
-  __syncwarp();
+  return __shfl_sync(0xffffffffu, ok, 0) != 0;
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -183,7 +197,9 @@ __host__ __device__ inline size_t ws_smem_bytes(int Dp, int KC, int BW) {
   return off;
 }
 
-template <typename TA, typename TW, int CELL, int NT, int U, int XR>
+// STREAM: X arrives while the kernel runs (rnnb_forward_host streaming); a
+// separate instantiation so the plain kernel's code is untouched.
+template <typename TA, typename TW, int CELL, int NT, int U, int XR, bool STREAM = false>
 __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
     ffma_ws_kernel(LayerArgs<TA, TW> a, const __grid_constant__ CUtensorMap tmx) {
   using C = WsCfg<TA, TW, CELL, NT, U>;
@@ -254,6 +270,9 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
   if (warp == CW) {
     // ---------------- producer: TMA bulk copies of x-row chunks ----------------
     uint32_t seq = 0;
+    bool timed_out = false;
+    uint64_t t_start = 0;
+    if constexpr (STREAM) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       for (int p0 = 0; p0 < l; p0 += NT) {
@@ -264,7 +283,10 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           const uint32_t ph = (seq / STAGES) & 1;
           if (a.dbg & 1) continue;
           mbar_wait_sleep(&empty[s], ph ^ 1);
-          if (a.x_ready != nullptr && ch == 0) wait_rows(a.x_ready, (int)((tp + NT) < a.L ? (tp + NT) : a.L));
+          if constexpr (STREAM) {
+            if (ch == 0 && !timed_out)
+              timed_out = !wait_rows(a.x_ready, (int)((tp + NT) < a.L ? (tp + NT) : a.L), t_start, a.stream_fail);
+          }
           const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
           const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
           TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
@@ -342,9 +364,11 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           }
         }
         epi_bar_sync();
-        if (a.h_done != nullptr && et == 0 && ((tp + nt) % a.h_chunk == 0 || tp + nt == a.L)) {
-          __threadfence();  // this CTA's h rows of the chunk (ordered by the barrier) before the count
-          atomicAdd(&a.h_done[(tp + nt - 1) / a.h_chunk], 1);
+        if constexpr (STREAM) {
+          if (et == 0 && ((tp + nt) % a.h_chunk == 0 || tp + nt == a.L)) {
+            __threadfence();  // this CTA's h rows of the chunk (ordered by the barrier) before the count
+            atomicAdd(&a.h_done[(tp + nt - 1) / a.h_chunk], 1);
+          }
         }
       }
     }

@@ -75,7 +75,8 @@ struct rnnb_stack {
   cudaEvent_t ev[2 * 8 + 2] = {};
   // streaming forward_host (single-layer fp32 stacks): counters the copy
   // streams and the layer kernel hand rows through
-  int* stream_ctr = nullptr;  // [0] rows of X resident, [1..] per-chunk CTA counts
+  int* stream_ctr = nullptr;  // [0] rows of X resident, [1] kernel time-out flag, [2..] per-chunk CTA counts
+  int* stream_flag_host = nullptr;  // pinned copy of the time-out flag
   const int* stream_ready = nullptr;
   int* stream_done = nullptr;
   int stream_chunk = 0;
@@ -85,6 +86,7 @@ struct rnnb_stack {
 namespace {
 
 constexpr int64_t kMaxStreamChunks = 64;
+bool g_stream_disabled = false;  // set after a streaming time-out (see rnnb_forward_host)
 
 // Stream memory operations (driver API, fetched through the runtime so the
 // library does not link libcuda): write a 32-bit value / wait for one.
@@ -166,6 +168,7 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
   a.xround = h->mode == RNNB_BF16 ? XR_BF16 : (h->mode == RNNB_TF32 ? XR_TF32 : XR_NONE);
   a.x_ready = h->stream_ready;
   a.h_done = h->stream_done;
+  a.stream_fail = h->stream_ready ? h->stream_ctr + 1 : nullptr;
   a.h_chunk = h->stream_chunk;
   return a;
 }
@@ -442,6 +445,7 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   if (h->stream_ctr) cudaFree(h->stream_ctr);
+  if (h->stream_flag_host) cudaFreeHost(h->stream_flag_host);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
   cudaSetDevice(cur);
@@ -647,7 +651,8 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
   // whose h rows it has stored, so the copy-out stream (stream wait-value)
   // drains chunk i while later chunks compute.
   const char* env_s = getenv("RNNB_HOST_STREAM");
-  const bool want_stream = !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
+  const bool want_stream =
+      !g_stream_disabled && !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
   StreamOps so = stream_ops();
   if (want_stream && so.write && so.wait) {
     // chunk: whole blocks, >= 128 steps, at most kMaxStreamChunks of them
@@ -656,13 +661,16 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
     sc = (sc + T - 1) / T * T;
     const int64_t nsc = (L + sc - 1) / sc;
     if (nsc <= kMaxStreamChunks) {
-      if (!h->stream_ctr) CUDA_TRY(cudaMalloc(&h->stream_ctr, (1 + kMaxStreamChunks) * sizeof(int)));
-      CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (1 + nsc) * sizeof(int), s));
+      if (!h->stream_ctr) {
+        CUDA_TRY(cudaMalloc(&h->stream_ctr, (2 + kMaxStreamChunks) * sizeof(int)));
+        CUDA_TRY(cudaHostAlloc(&h->stream_flag_host, sizeof(int), cudaHostAllocDefault));
+      }
+      CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (2 + nsc) * sizeof(int), s));
       CUDA_TRY(cudaEventRecord(ev_start, s));
       CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
       CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
       h->stream_ready = h->stream_ctr;
-      h->stream_done = h->stream_ctr + 1;
+      h->stream_done = h->stream_ctr + 2;
       h->stream_chunk = (int)sc;
       h->stream_refused = false;
       st = rnnb_forward(h, dX, din, L, block_size, dH, dh, dC, dXC, stream);
@@ -678,17 +686,26 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
         }
         for (int64_t i = 0; i < nsc; ++i) {
           const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
-          CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 1 + i), grid, CU_STREAM_WAIT_VALUE_GEQ));
+          CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 2 + i), grid, CU_STREAM_WAIT_VALUE_GEQ));
           CUDA_TRY(cudaMemcpyAsync(hH + t0 * dh * es, dH + t0 * dh * es, n * dh * es, cudaMemcpyDeviceToHost,
                                    h->s_out));
         }
         CUDA_TRY(cudaEventRecord(ev_done, h->s_out));
         CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
-        if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
-        if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(h->stream_flag_host, h->stream_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
         CUDA_TRY(cudaStreamSynchronize(s));
+        if (*h->stream_flag_host == 0) {
+          if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
+          if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
+          CUDA_TRY(cudaStreamSynchronize(s));
+          if (cur != h->device) cudaSetDevice(cur);
+          return st;
+        }
+        // the rows did not arrive while the kernel waited (a serialising
+        // profiler, a stalled copy engine): redo the call without streaming
         if (cur != h->device) cudaSetDevice(cur);
-        return st;
+        g_stream_disabled = true;  // do not try streaming again in this process
+        return rnnb_forward_host(h, X, L, block_size, H, c_state, x_carry, stream);
       }
       if (!h->stream_refused) {
         if (cur != h->device) cudaSetDevice(cur);
