@@ -3,10 +3,10 @@
 # timings, ncu launch list, one full ncu capture of the headline kernel and the
 # per-T_b counter sweep.  Outputs under gpurun_out/ (copy what is judged to profiles/).
 set -x
-python bench.py > gpurun_out/bench_r1c.json 2> gpurun_out/bench_r1c.err
-python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_c.json 2>&1
-python tools/bench_configs.py --out gpurun_out/configs_c.json > gpurun_out/configs_c.log 2>&1
+python bench.py > gpurun_out/bench_r1e.json 2> gpurun_out/bench_r1e.err
+python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref_e.json 2>&1
+python tools/bench_configs.py --out gpurun_out/configs_e.json > gpurun_out/configs_e.log 2>&1
 python bench.py --steps 2 --warmup 3 --no-sweep --extra-modes '' --no-cpu-baseline > gpurun_out/b_small.json 2>&1 && \
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c.csv python bench.py --steps 2 --warmup 3 --no-sweep --extra-modes '' --no-cpu-baseline > gpurun_out/ncu_l.log 2>&1
-python tools/run_once.py --reps 1 > /dev/null && ncu --set full --import-source on --clock-control none -k regex:ffma_ws -c 1 -f -o gpurun_out/prof_r1c_ffma_cfg2_T32 python tools/run_once.py --reps 1 > gpurun_out/ncu_f.log 2>&1
-bash tools/ncu_sweep.sh gpurun_out/ncu_sweep_c > gpurun_out/ncu_sweep_c.log 2>&1
+  RNNB_HOST_STREAM=0 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_e.csv python bench.py --steps 2 --warmup 3 --no-sweep --extra-modes '' --no-cpu-baseline > gpurun_out/ncu_l.log 2>&1
+python tools/run_once.py --reps 1 > /dev/null && ncu --set full --import-source on --clock-control none -k regex:ffma_ws -c 1 -f -o gpurun_out/prof_r1e_ffma_cfg2_T32 python tools/run_once.py --reps 1 > gpurun_out/ncu_f.log 2>&1
+bash tools/ncu_sweep.sh gpurun_out/ncu_sweep_e > gpurun_out/ncu_sweep_e.log 2>&1
