@@ -66,6 +66,12 @@ def lib():
             f = getattr(L, f"orc_gemv_ref_{sfx}")
             f.argtypes = [vp, vp, vp, i64, i64]
             f.restype = None
+            f = getattr(L, f"orc_lstm_blocked_{sfx}")
+            f.argtypes = [i64, i64, vp, vp, i64, i64, ci, vp, vp, vp]
+            f.restype = ci
+            f = getattr(L, f"orc_lstm_stepwise_{sfx}")
+            f.argtypes = [i64, i64, vp, vp, i64, vp, vp, vp]
+            f.restype = ci
         L.orc_sm64_fill.argtypes = [ctypes.c_uint64, vp, i64]
         L.orc_uniform.argtypes = [vp, vp, i64]
         L.orc_set_threads.argtypes = [ci]
@@ -216,7 +222,9 @@ def uniform_array(raws):
 
 
 def layer_spec(kind, d_in, d_h):
-    """model_io.py:133-139 (SRU/QRNN rows)."""
+    """model_io.py:133-139."""
+    if str(getattr(kind, "value", kind)).lower() == "lstm":
+        return [(d_h, d_in)] * 4 + [(d_h, d_h)] * 4 + [(d_h,)] * 4
     if kind_code(kind) == SRU:
         return [(d_h, d_in)] * 3 + [(d_h,)] * 2
     return [(d_h, d_in)] * 6
@@ -244,3 +252,52 @@ def generate_layers(kind, d_in, d_h, n_layers, seed, dtype):
 def generate_sequence(seq_len, width, seed, dtype):
     """model_io.py:180-188."""
     return uniform_array(raw_stream(seed, seq_len * width)).astype(dtype).reshape(seq_len, width)
+
+
+# ---------------------------------------------------------------------------
+# LSTM (SURVEY.md §8f rank 1)
+
+LSTM_FIELDS = ("w_forget", "w_input", "w_output", "w_cand", "u_forget", "u_input", "u_output", "u_cand",
+               "b_forget", "b_input", "b_output", "b_cand")
+
+
+def lstm_mats(w, dtype):
+    if isinstance(w, (list, tuple)):
+        mats = list(w)
+    elif isinstance(w, dict):
+        mats = [w[f] for f in LSTM_FIELDS]
+    else:
+        mats = [getattr(w, f) for f in LSTM_FIELDS]
+    return [np.ascontiguousarray(m, dtype=dtype) for m in mats]
+
+
+def _lstm(fn, w, X, *extra, c=None, h=None):
+    X = np.ascontiguousarray(X)
+    mats = lstm_mats(w, X.dtype)
+    dh, din = mats[0].shape
+    if X.ndim != 2 or X.shape[1] != din:
+        raise ValueError(f"input must be [L x {din}], got {X.shape}")
+    H = np.empty((X.shape[0], dh), X.dtype)
+    arr = (ctypes.c_void_p * 12)(*[m.ctypes.data for m in mats])
+    c_buf = np.zeros(dh, X.dtype) if c is None else np.ascontiguousarray(c, dtype=X.dtype).copy()
+    h_buf = np.zeros(dh, X.dtype) if h is None else np.ascontiguousarray(h, dtype=X.dtype).copy()
+    rc = fn(din, dh, arr, _ptr(X), X.shape[0], *extra, _ptr(H), _ptr(c_buf), _ptr(h_buf))
+    if rc != 0:
+        raise ValueError("oracle rejected the arguments")
+    return H, c_buf, h_buf
+
+
+def lstm_blocked(w, X, block_size, kernel="fast", c=None, h=None, return_state=False):
+    """lstm_run_precomputed (blocked.py:271-305); returns H (and c_T, h_T)."""
+    if block_size < 1:
+        raise ValueError("block_size must be >= 1")
+    fn = getattr(lib(), f"orc_lstm_blocked_{_sfx(X.dtype)}")
+    H, c, h = _lstm(fn, w, X, int(block_size), KERNELS[kernel], c=c, h=h)
+    return (H, c, h) if return_state else H
+
+
+def lstm_stepwise(w, X, c=None, h=None, return_state=False):
+    """lstm_step (cells.py:153-164) over the sequence, strict gemv."""
+    fn = getattr(lib(), f"orc_lstm_stepwise_{_sfx(X.dtype)}")
+    H, c, h = _lstm(fn, w, X, c=c, h=h)
+    return (H, c, h) if return_state else H

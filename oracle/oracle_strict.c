@@ -248,3 +248,93 @@ void orc_uniform(const uint64_t *raw, double *out, int64_t n)
 
 ORC_DEFINE(float, f32, tanhf)
 ORC_DEFINE(double, f64, tanh)
+
+/* ---- LSTM, instantiated for float and double ----
+ * mats (cells.py:46-58, model_io.py:29-33): w_forget, w_input, w_output,
+ * w_cand [dh x din], u_forget, u_input, u_output, u_cand [dh x dh],
+ * b_forget, b_input, b_output, b_cand [dh].  Gate slot g: 0 f, 1 i, 2 o, 3 c.
+ * c_io / h_io: optional state in and out (zero when NULL, as the
+ * reference's h = c = 0 at blocked.py:284-285 / cells.py:138-143). */
+#define ORC_DEFINE_LSTM(T, SFX, TANH)                                                      \
+    /* lstm_run_precomputed, blocked.py:271-305: per block the four W Xb products +   */  \
+    /* bias ((W x) + b), then per step pre = that + U h_{t-1} (strict gemv order).     */  \
+    int orc_lstm_blocked_##SFX(int64_t din, int64_t dh, const T *const *mats, const T *Xin, \
+                               int64_t L, int64_t Tb, int kernel, T *Hout, T *c_io, T *h_io) \
+    {                                                                                      \
+        if (L < 1 || Tb < 1 || din < 1 || dh < 1) return -1;                               \
+        int64_t nb = Tb < L ? Tb : L;                                                      \
+        T *Xb = malloc(sizeof(T) * din * nb), *Xbt = malloc(sizeof(T) * din * nb);         \
+        T *g[4];                                                                           \
+        for (int q = 0; q < 4; ++q) g[q] = malloc(sizeof(T) * dh * nb);                    \
+        T *u = malloc(sizeof(T) * dh), *act = malloc(sizeof(T) * 4 * dh);                  \
+        T *c = calloc(dh, sizeof(T)), *h = calloc(dh, sizeof(T));                          \
+        if (c_io) memcpy(c, c_io, sizeof(T) * dh);                                         \
+        if (h_io) memcpy(h, h_io, sizeof(T) * dh);                                         \
+        for (int64_t s = 0; s < L; s += Tb) {                                              \
+            int64_t l = (L - s) < Tb ? (L - s) : Tb;                                       \
+            for (int64_t t = 0; t < l; ++t)                                                \
+                for (int64_t i = 0; i < din; ++i) {                                        \
+                    Xb[i * l + t] = Xin[(s + t) * din + i];                                \
+                    Xbt[t * din + i] = Xin[(s + t) * din + i];                             \
+                }                                                                          \
+            for (int q = 0; q < 4; ++q) {                                                  \
+                gemm_##SFX(mats[q], Xb, Xbt, g[q], dh, din, l, kernel);                    \
+                for (int64_t i = 0; i < dh; ++i)                                           \
+                    for (int64_t t = 0; t < l; ++t) g[q][i * l + t] += mats[8 + q][i];     \
+            }                                                                              \
+            for (int64_t t = 0; t < l; ++t) {                                              \
+                for (int q = 0; q < 4; ++q) {                                              \
+                    orc_gemv_ref_##SFX(mats[4 + q], h, u, dh, dh);                         \
+                    for (int64_t i = 0; i < dh; ++i) {                                     \
+                        T z = g[q][i * l + t] + u[i];                                      \
+                        act[q * dh + i] = q == 3 ? TANH(z) : sig_##SFX(z);                 \
+                    }                                                                      \
+                }                                                                          \
+                for (int64_t i = 0; i < dh; ++i) {                                         \
+                    c[i] = act[i] * c[i] + act[dh + i] * act[3 * dh + i];                  \
+                    h[i] = act[2 * dh + i] * TANH(c[i]);                                   \
+                    Hout[(s + t) * dh + i] = h[i];                                         \
+                }                                                                          \
+            }                                                                              \
+        }                                                                                  \
+        if (c_io) memcpy(c_io, c, sizeof(T) * dh);                                         \
+        if (h_io) memcpy(h_io, h, sizeof(T) * dh);                                         \
+        free(Xb); free(Xbt); free(u); free(act); free(c); free(h);                         \
+        for (int q = 0; q < 4; ++q) free(g[q]);                                            \
+        return 0;                                                                          \
+    }                                                                                      \
+                                                                                           \
+    /* lstm_step, cells.py:153-164: sigma(W x + U h + b) per gate, strict gemv. */         \
+    int orc_lstm_stepwise_##SFX(int64_t din, int64_t dh, const T *const *mats, const T *Xin, \
+                                int64_t L, T *Hout, T *c_io, T *h_io)                      \
+    {                                                                                      \
+        if (L < 1 || din < 1 || dh < 1) return -1;                                         \
+        T *a = malloc(sizeof(T) * dh), *b = malloc(sizeof(T) * dh);                        \
+        T *act = malloc(sizeof(T) * 4 * dh);                                               \
+        T *c = calloc(dh, sizeof(T)), *h = calloc(dh, sizeof(T));                          \
+        if (c_io) memcpy(c, c_io, sizeof(T) * dh);                                         \
+        if (h_io) memcpy(h, h_io, sizeof(T) * dh);                                         \
+        for (int64_t t = 0; t < L; ++t) {                                                  \
+            const T *x = Xin + t * din;                                                    \
+            for (int q = 0; q < 4; ++q) {                                                  \
+                orc_gemv_ref_##SFX(mats[q], x, a, dh, din);                                \
+                orc_gemv_ref_##SFX(mats[4 + q], h, b, dh, dh);                             \
+                for (int64_t i = 0; i < dh; ++i) {                                         \
+                    T z = a[i] + b[i] + mats[8 + q][i];                                    \
+                    act[q * dh + i] = q == 3 ? TANH(z) : sig_##SFX(z);                     \
+                }                                                                          \
+            }                                                                              \
+            for (int64_t i = 0; i < dh; ++i) {                                             \
+                c[i] = act[i] * c[i] + act[dh + i] * act[3 * dh + i];                      \
+                h[i] = act[2 * dh + i] * TANH(c[i]);                                       \
+                Hout[t * dh + i] = h[i];                                                   \
+            }                                                                              \
+        }                                                                                  \
+        if (c_io) memcpy(c_io, c, sizeof(T) * dh);                                         \
+        if (h_io) memcpy(h_io, h, sizeof(T) * dh);                                         \
+        free(a); free(b); free(act); free(c); free(h);                                     \
+        return 0;                                                                          \
+    }
+
+ORC_DEFINE_LSTM(float, f32, tanhf)
+ORC_DEFINE_LSTM(double, f64, tanh)

@@ -21,7 +21,9 @@ and writes:
                            f32/f64 and stacks;
 * ``baseline_cfg.npz``  -- the reference on BASELINE cfg1 (full) and cfg2
                            (c_T + row subsample), inputs from
-                           paper_1803_11389_b200.workloads (seeded PCG64).
+                           paper_1803_11389_b200.workloads (seeded PCG64);
+* ``lstm_cases.npz``    -- lstm_run_precomputed / run_stepwise on seeded
+                           LSTM layers (weights and inputs included).
 """
 
 import json
@@ -105,6 +107,21 @@ def cells_d2():
         "X": Xq.tolist(), "H": Hq.tolist(), "C": cs,
         "golden_published": tc.QRNN_GOLDEN,
     }
+    lw = tc.lstm_w2()
+    Xl = np.array([[0.5, -0.3], [-0.4, 0.2]], np.float64)
+    st = rbc.zero_state(2, 2, np.float64)
+    hs, cs = [], []
+    for x in Xl:
+        st = rbc.lstm_step(lw, x, st)
+        hs.append(st.h.tolist())
+        cs.append(st.c.tolist())
+    out["lstm"] = {
+        "weights": {k: getattr(lw, k).tolist() for k in LSTM_FIELDS},
+        "X": Xl.tolist(), "H": hs, "C": cs,
+        "H_precomputed_T1": rbb.lstm_run_precomputed(lw, Xl, 1).tolist(),
+        "H_precomputed_T2": rbb.lstm_run_precomputed(lw, Xl, 2).tolist(),
+        "golden_published": tc.LSTM_GOLDEN,
+    }
     with open(os.path.join(HERE, "cells_d2.json"), "w") as f:
         json.dump(out, f, indent=1)
 
@@ -137,6 +154,39 @@ CASES = [
     ("qrnn", "f32", 33, 70, 2, (7, 32)),
 ]
 WSEED, XSEED = 42, 43
+
+LSTM_FIELDS = ("w_forget", "w_input", "w_output", "w_cand", "u_forget", "u_input", "u_output", "u_cand",
+               "b_forget", "b_input", "b_output", "b_cand")
+LSTM_CASES = [
+    # precision, d_in, d_h, L, T_b list
+    ("f32", 8, 8, 16, (1, 4, 16)),
+    ("f32", 64, 64, 128, (1, 16, 128)),
+    ("f32", 96, 160, 75, (8, 32)),
+    ("f64", 32, 48, 40, (1, 7)),
+    ("f32", 350, 350, 64, (16,)),
+]
+
+
+def lstm_cases():
+    """lstm_run_precomputed (kernel="fast") per T_b and run_stepwise for
+    seeded LSTM layers (weights generated by the reference)."""
+    arrays, index = {}, []
+    for n, (prec, din, dh, L, Tbs) in enumerate(LSTM_CASES):
+        cfg = rb.RnnConfig(rbc.CellKind.LSTM, din, dh, n_layers=1, precision=prec)
+        ws = rb.generate_weights(cfg, 700 + n)
+        X = rb.generate_sequence(L, din, 800 + n, prec)
+        if din * dh <= 160 * 160:  # larger weight sets are regenerated by the oracle's SplitMix64 restatement
+            for f in LSTM_FIELDS:
+                arrays[f"l{n}_{f}"] = getattr(ws.layers[0], f)
+        arrays[f"l{n}_X"] = X
+        arrays[f"l{n}_stepwise"] = rb.run_stepwise(cfg, ws, X)
+        for T in Tbs:
+            arrays[f"l{n}_T{T}_H"] = rbb.lstm_run_precomputed(ws.layers[0], X, T, kernel="fast")
+        index.append({"case": n, "precision": prec, "d_in": din, "d_h": dh, "L": L, "T_b": list(Tbs),
+                      "wseed": 700 + n, "xseed": 800 + n})
+    np.savez_compressed(os.path.join(HERE, "lstm_cases.npz"), **arrays)
+    with open(os.path.join(HERE, "lstm_cases.json"), "w") as f:
+        json.dump(index, f, indent=1)
 
 
 def blocked_cases():
@@ -187,8 +237,7 @@ def baseline_cfgs():
 
 
 if __name__ == "__main__":
-    cells_d2()
-    splitmix()
-    blocked_cases()
-    baseline_cfgs()
-    print("golden fixtures written to", HERE)
+    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases"]
+    for part in parts:
+        globals()[part]()
+    print("golden fixtures written to", HERE, parts)

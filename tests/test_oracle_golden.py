@@ -124,3 +124,46 @@ def test_oracle_baseline_cfg1_against_reference(oracle):
         if T == 16:
             ref = g["cfg1_T16_H"]
             assert np.max(np.abs(H - ref)) / np.max(np.abs(ref)) <= 1e-6
+
+
+# ---------------------------------------------------------------------------
+# LSTM partial precompute (blocked.py:271-305, cells.py:153-164)
+
+
+def test_lstm_d2_golden_vectors(oracle):
+    """The reference suite's hand-checked d=2 LSTM goldens (test_cells.py
+    LSTM_GOLDEN, 1e-12) through both oracle paths."""
+    g = _json("cells_d2.json")["lstm"]
+    w = [np.array(g["weights"][f], np.float64) for f in oracle.LSTM_FIELDS]
+    X = np.array(g["X"], np.float64)
+    H, c, h = oracle.lstm_stepwise(w, X, return_state=True)
+    for t, (h_exp, c_exp) in enumerate(g["golden_published"]):
+        assert np.max(np.abs(H[t] - h_exp)) < 1e-12
+    assert np.max(np.abs(c - g["golden_published"][-1][1])) < 1e-12
+    for T in (1, 2):
+        Hb = oracle.lstm_blocked(w, X, T, kernel="reference")
+        assert np.max(np.abs(Hb - np.array(g[f"H_precomputed_T{T}"]))) < 1e-15
+
+
+def _lstm_cases():
+    return _json("lstm_cases.json")
+
+
+@pytest.mark.parametrize("case", _lstm_cases(), ids=lambda c: f"{c['precision']}-{c['d_in']}x{c['d_h']}-L{c['L']}")
+def test_oracle_matches_reference_lstm(oracle, case):
+    """lstm_run_precomputed (kernel='fast') and run_stepwise outputs made by
+    the reference; weights regenerated by the oracle's SplitMix64
+    restatement where the fixture omits them (checked equal where present)."""
+    z = np.load(os.path.join(GOLDEN, "lstm_cases.npz"))
+    n = case["case"]
+    dt = np.float32 if case["precision"] == "f32" else np.float64
+    gen = oracle.generate_layers("lstm", case["d_in"], case["d_h"], 1, case["wseed"], dt)[0]
+    if f"l{n}_w_forget" in z:
+        ref_w = [z[f"l{n}_{f}"] for f in oracle.LSTM_FIELDS]
+        assert all(np.array_equal(a, b) for a, b in zip(ref_w, gen))
+    X = z[f"l{n}_X"]
+    assert np.array_equal(X, oracle.generate_sequence(case["L"], case["d_in"], case["xseed"], dt))
+    tol = 1e-6 if dt == np.float32 else 1e-14
+    assert np.max(np.abs(oracle.lstm_stepwise(gen, X) - z[f"l{n}_stepwise"])) <= tol
+    for T in case["T_b"]:
+        assert np.max(np.abs(oracle.lstm_blocked(gen, X, T) - z[f"l{n}_T{T}_H"])) <= tol
