@@ -130,6 +130,32 @@ rnnb_status rnnb_sweep(const void* forget, const void* cand, const void* c_init,
 rnnb_status rnnb_finalize(int kind, const void* out_gate, const void* C, const void* Xb, void* H,
                           int64_t d, int64_t T, int dtype, void* stream);
 
+/* ---- LSTM partial precompute ----
+ * lstm_run_precomputed(w, X, block_size)  blocked.py:271-305, one layer:
+ * input-side products W x + b for the sequence (one GEMM launch), then the
+ * recurrence in one persistent cooperative launch with each CTA's rows of
+ * U resident in shared memory.  Modes RNNB_F32 / RNNB_F64 (the reference's
+ * precisions).  Blocks only decide where the reference batches W x, never
+ * its value; block_size is validated like plan_blocks. */
+typedef struct rnnb_lstm* rnnb_lstm_t;
+rnnb_status rnnb_lstm_create(rnnb_lstm_t* out, int64_t d_in, int64_t d_h, int mode, int device);
+rnnb_status rnnb_lstm_destroy(rnnb_lstm_t h);
+/* mats[12] HOST row-major in the reference's field order (cells.py:46-58,
+ * model_io.py:29-33): w_forget, w_input, w_output, w_cand [d_h x d_in],
+ * u_forget, u_input, u_output, u_cand [d_h x d_h], b_forget, b_input,
+ * b_output, b_cand [d_h]. */
+rnnb_status rnnb_lstm_set_weights(rnnb_lstm_t h, const void* const* mats, int n_mats, int src_dtype);
+/* DEVICE buffers: X [L x d_in] (row stride ldx) -> H [L x d_h] (ldh);
+ * c_state, h_state optional [d_h] in/out (NULL: zero in, not written). */
+rnnb_status rnnb_lstm_forward(rnnb_lstm_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size,
+                              void* H, int64_t ldh, void* c_state, void* h_state, void* stream);
+/* Same on HOST buffers (copies inside the call; synchronises the stream). */
+rnnb_status rnnb_lstm_forward_host(rnnb_lstm_t h, const void* X, int64_t L, int64_t block_size, void* H,
+                                   void* c_state, void* h_state, void* stream);
+/* what: 0 weight bytes, 1 launches of the last forward, 2 units per CTA,
+ * 3 = 1 if the CTA's U rows were shared-memory resident, 4 grid size. */
+rnnb_status rnnb_lstm_query(rnnb_lstm_t h, int what, int64_t* value);
+
 /* Introspection for benches/tests. what: 0 = device weight bytes,
  * 1 = kernel launches issued by the last forward, 2 = units per CTA of
  * `layer`, 3 = 1 if the last forward kept `layer`'s weights resident in

@@ -7,6 +7,7 @@ hand-written sm_100a CUDA kernels in ``librnnb.so`` behind a C ABI
 
 Fast path: ``DeviceStack`` (weights resident in HBM, forward on device
 tensors).  Drop-in path: ``run_blocked(cfg, weights, X, block_size)``.
+LSTM partial precompute: ``lstm_run_precomputed`` / ``DeviceLstm``.
 """
 
 from .blocked import (
@@ -29,13 +30,14 @@ from .cells import (
     PRECISIONS,
     CellKind,
     CellState,
+    LstmWeights,
     QrnnWeights,
     RnnConfig,
     SruWeights,
     WeightSet,
     zero_state,
 )
-from .device import DeviceStack
+from .device import DeviceLstm, DeviceStack
 
 __version__ = "0.1.0"
 
@@ -44,5 +46,5 @@ __all__ = [
     "TraceEvent", "finalize_outputs", "lstm_run_precomputed", "plan_blocks",
     "precompute_gates_qrnn", "precompute_gates_sru", "recurrence_sweep", "run_blocked",
     "PRECISIONS", "CellKind", "CellState", "QrnnWeights", "RnnConfig", "SruWeights",
-    "WeightSet", "zero_state", "DeviceStack",
+    "WeightSet", "zero_state", "DeviceStack", "LstmWeights", "DeviceLstm",
 ]

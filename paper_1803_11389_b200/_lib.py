@@ -21,7 +21,8 @@ SYMBOLS = (
     "rnnb_last_error", "rnnb_version", "rnnb_plan_blocks", "rnnb_stack_create",
     "rnnb_stack_destroy", "rnnb_stack_set_layer", "rnnb_forward", "rnnb_forward_host",
     "rnnb_gates", "rnnb_sweep", "rnnb_finalize", "rnnb_query", "rnnb_stack_create_ex",
-    "rnnb_stack_set_highway",
+    "rnnb_stack_set_highway", "rnnb_lstm_create", "rnnb_lstm_destroy", "rnnb_lstm_set_weights",
+    "rnnb_lstm_forward", "rnnb_lstm_forward_host", "rnnb_lstm_query",
 )
 FLAG_WIDE_SRU = 1
 
@@ -58,6 +59,12 @@ def load():
         "rnnb_sweep": ([vp, vp, vp, vp, i64, i64, ci, vp], ci),
         "rnnb_finalize": ([ci, vp, vp, vp, vp, i64, i64, ci, vp], ci),
         "rnnb_query": ([vp, ci, ci, P64], ci),
+        "rnnb_lstm_create": ([ctypes.POINTER(vp), i64, i64, ci, ci], ci),
+        "rnnb_lstm_destroy": ([vp], ci),
+        "rnnb_lstm_set_weights": ([vp, ctypes.POINTER(vp), ci, ci], ci),
+        "rnnb_lstm_forward": ([vp, vp, i64, i64, i64, vp, i64, vp, vp, vp], ci),
+        "rnnb_lstm_forward_host": ([vp, vp, i64, i64, vp, vp, vp, vp], ci),
+        "rnnb_lstm_query": ([vp, ci, P64], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

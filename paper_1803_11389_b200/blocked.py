@@ -26,8 +26,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .cells import CellKind
-from .device import DeviceStack, _stream_ptr
+from .cells import LSTM_FIELDS, CellKind, LstmWeights
+from .device import DeviceLstm, DeviceStack, _stream_ptr
 
 KERNELS = ("reference", "tiled", "fast")
 
@@ -316,7 +316,40 @@ def run_blocked(cfg, weights, X: np.ndarray, block_size: int, kernel: str = "fas
     return out, cs, xcs
 
 
-def lstm_run_precomputed(*args, **kwargs):
-    """LSTM partial precompute (blocked.py:271-305) is outside this build's
-    hot path."""
-    raise NotImplementedError("LSTM partial precompute is not part of the B200 blocked path yet")
+def lstm_run_precomputed(w: LstmWeights, X: np.ndarray, block_size: int, kernel: str = "fast",
+                         trace: KernelTrace = None) -> np.ndarray:
+    """LSTM with the input-side products batched (blocked.py:271-305).
+
+    Same signature, validation, trace events and result as the reference: per
+    block the four W x products + biases (GEMM + BIAS events), per step the
+    four U h products (GEMV events).  On the GPU the input-side products of
+    the whole sequence are one GEMM launch (blocks only decide where the
+    reference batches them, never their values) and the recurrence is one
+    persistent launch with U resident in shared memory.
+    """
+    if X.ndim != 2 or X.shape[1] != w.d_in:
+        raise ValueError(f"input must be [L x {w.d_in}], got {X.shape}")
+    plan = plan_blocks(X.shape[0], block_size)
+    _check_kernel(kernel)
+    for f in LSTM_FIELDS:
+        a = np.asarray(getattr(w, f))
+        if a.dtype != X.dtype:
+            raise ValueError(f"dtype mismatch: {a.dtype} vs {X.dtype}")
+        if a.ndim == 2:
+            _check_matrix(a, f)
+    mode = _mode_for(X.dtype)
+    if trace is not None:
+        for _, length in plan.blocks:
+            for wm, bv in ((w.w_forget, w.b_forget), (w.w_input, w.b_input), (w.w_output, w.b_output),
+                           (w.w_cand, w.b_cand)):
+                trace.add(PHASE_GEMM, wm.shape[0], wm.shape[1], length)
+                trace.add(PHASE_BIAS, bv.shape[0], 1, length)
+            for _ in range(length):
+                for _ in range(4):
+                    trace.add(PHASE_GEMV, w.d_h, w.d_h, 1)
+    dev = DeviceLstm(w, mode=mode)
+    try:
+        out = dev.forward_host(np.ascontiguousarray(X), block_size)
+    finally:
+        dev.close()
+    return out.astype(X.dtype, copy=False)

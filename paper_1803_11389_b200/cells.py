@@ -9,8 +9,9 @@ reference package's types, so reference callers keep working:
 * ``CellState`` / ``zero_state``   -- cells.py:129-143
 * ``RnnConfig`` / ``WeightSet``    -- model_io.py:75-110
 
-LSTM weights are accepted by ``CellKind`` only so that the blocked entry
-point can reject them the way the reference does (blocked.py:231-233).
+* ``LstmWeights``                 -- cells.py:46-75 (for lstm_run_precomputed;
+                                     the blocked entry point rejects LSTM the
+                                     way the reference does, blocked.py:231-233)
 """
 
 from dataclasses import dataclass, field
@@ -40,7 +41,48 @@ def _expect(cond, msg):
 
 
 SRU_FIELDS = ("w_cand", "w_forget", "w_highway", "b_forget", "b_highway")
+LSTM_FIELDS = ("w_forget", "w_input", "w_output", "w_cand", "u_forget", "u_input", "u_output", "u_cand",
+               "b_forget", "b_input", "b_output", "b_cand")
 QRNN_FIELDS = ("w_cand", "w_cand_prev", "w_forget", "w_forget_prev", "w_out", "w_out_prev")
+
+
+@dataclass
+class LstmWeights:
+    """f, i, o = sigma(W x + U h + b); cand = tanh(W_c x + U_c h + b_c);
+    c = f c + i cand; h = o tanh(c) (cells.py:153-164)."""
+
+    w_forget: np.ndarray
+    w_input: np.ndarray
+    w_output: np.ndarray
+    w_cand: np.ndarray
+    u_forget: np.ndarray
+    u_input: np.ndarray
+    u_output: np.ndarray
+    u_cand: np.ndarray
+    b_forget: np.ndarray
+    b_input: np.ndarray
+    b_output: np.ndarray
+    b_cand: np.ndarray
+
+    def __post_init__(self):
+        d_h, d_in = self.w_forget.shape
+        for w in (self.w_input, self.w_output, self.w_cand):
+            _expect(w.shape == (d_h, d_in), "input-side weight shapes disagree")
+        for u in (self.u_forget, self.u_input, self.u_output, self.u_cand):
+            _expect(u.shape == (d_h, d_h), "recurrent weights must be square d_h x d_h")
+        for b in (self.b_forget, self.b_input, self.b_output, self.b_cand):
+            _expect(b.shape == (d_h,), "bias length must equal d_h")
+
+    @property
+    def d_in(self):
+        return self.w_forget.shape[1]
+
+    @property
+    def d_h(self):
+        return self.w_forget.shape[0]
+
+    def mats(self):
+        return tuple(getattr(self, f) for f in LSTM_FIELDS)
 
 
 @dataclass

@@ -22,6 +22,15 @@ rnnb_status fail(rnnb_status s, const std::string& msg) {
 rnnb_status cuda_fail(cudaError_t e, const char* where) {
   return fail(RNNB_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
+}  // namespace
+
+namespace rnnb {
+// shared with lstm.cu: one thread-local last-error string per process
+rnnb_status set_error(rnnb_status s, const std::string& msg) { return fail(s, msg); }
+}  // namespace rnnb
+
+namespace {
+
 #define CUDA_TRY(expr)                                  \
   do {                                                  \
     cudaError_t _e = (expr);                            \

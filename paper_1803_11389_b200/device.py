@@ -12,7 +12,7 @@ import ctypes
 import numpy as np
 
 from . import _lib
-from .cells import CellKind, QRNN_FIELDS, SRU_FIELDS
+from .cells import CellKind, LSTM_FIELDS, QRNN_FIELDS, SRU_FIELDS
 
 
 def _torch():
@@ -169,6 +169,100 @@ class DeviceStack:
     def close(self):
         if getattr(self, "_h", None):
             self.lib.rnnb_stack_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+class DeviceLstm:
+    """One LSTM layer resident on one GPU (lstm_run_precomputed,
+    blocked.py:271-305): the input-side products for the sequence in one
+    GEMM launch, the recurrence in one persistent cooperative launch with
+    each CTA's rows of U in shared memory.  mode: "f32" | "f64"."""
+
+    def __init__(self, w, mode="f32", device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _lib.RnnbError("CUDA is not available: the LSTM path has no CPU fallback")
+        self.lib = _lib.load()
+        if mode not in ("f32", "f64"):
+            raise ValueError("LSTM modes are f32 and f64 (the reference precisions)")
+        self.mode = mode
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        mats = list(w) if isinstance(w, (list, tuple)) else [getattr(w, f) for f in LSTM_FIELDS]
+        self.d_h, self.d_in = (int(v) for v in np.shape(mats[0]))
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.rnnb_lstm_create(ctypes.byref(h), self.d_in, self.d_h, _lib.MODES[mode], self.device))
+        self._h = h
+        self.set_weights(mats)
+
+    @property
+    def dtype(self):
+        torch = _torch()
+        return torch.float64 if self.mode == "f64" else torch.float32
+
+    @property
+    def np_dtype(self):
+        return np.float64 if self.mode == "f64" else np.float32
+
+    def set_weights(self, mats):
+        src = self.np_dtype
+        arrs = [np.ascontiguousarray(np.asarray(m), dtype=src) for m in mats]
+        ptrs = (ctypes.c_void_p * len(arrs))(*[a.ctypes.data for a in arrs])
+        dt = _lib.DT_F64 if src is np.float64 else _lib.DT_F32
+        _lib.check(self.lib.rnnb_lstm_set_weights(self._h, ptrs, len(arrs), dt))
+
+    def forward(self, X, block_size, out=None, c_state=None, h_state=None, stream=None):
+        """X [L x d_in] CUDA tensor -> [L x d_h]; c_state / h_state optional
+        [d_h] CUDA tensors, in/out."""
+        torch = _torch()
+        if not isinstance(X, torch.Tensor) or not X.is_cuda or X.dim() != 2 or X.stride(1) != 1:
+            raise ValueError("X must be a 2-d row-major CUDA tensor")
+        if X.dtype != self.dtype:
+            raise ValueError(f"dtype mismatch: {X.dtype} vs {self.dtype}")
+        if X.shape[1] != self.d_in:
+            raise ValueError(f"input must be [L x {self.d_in}], got {tuple(X.shape)}")
+        L = X.shape[0]
+        if out is None:
+            out = torch.empty((L, self.d_h), dtype=self.dtype, device=X.device)
+        cp = ctypes.c_void_p(c_state.data_ptr()) if c_state is not None else None
+        hp = ctypes.c_void_p(h_state.data_ptr()) if h_state is not None else None
+        _lib.check(self.lib.rnnb_lstm_forward(self._h, ctypes.c_void_p(X.data_ptr()), X.stride(0), L,
+                                              int(block_size), ctypes.c_void_p(out.data_ptr()), out.stride(0),
+                                              cp, hp, _stream_ptr(stream)))
+        return out
+
+    def forward_host(self, X, block_size, out=None, c_state=None, h_state=None, stream=None):
+        X = np.ascontiguousarray(X, dtype=self.np_dtype)
+        if X.ndim != 2 or X.shape[1] != self.d_in:
+            raise ValueError(f"input must be [L x {self.d_in}], got {X.shape}")
+        if out is None:
+            out = np.empty((X.shape[0], self.d_h), self.np_dtype)
+        cp = c_state.ctypes.data_as(ctypes.c_void_p) if c_state is not None else None
+        hp = h_state.ctypes.data_as(ctypes.c_void_p) if h_state is not None else None
+        _lib.check(self.lib.rnnb_lstm_forward_host(self._h, X.ctypes.data_as(ctypes.c_void_p), X.shape[0],
+                                                   int(block_size), out.ctypes.data_as(ctypes.c_void_p),
+                                                   cp, hp, _stream_ptr(stream)))
+        return out
+
+    def query(self, what):
+        v = ctypes.c_int64()
+        _lib.check(self.lib.rnnb_lstm_query(self._h, what, ctypes.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.rnnb_lstm_destroy(self._h)
             self._h = None
 
     def __del__(self):
