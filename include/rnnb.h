@@ -47,7 +47,10 @@ typedef enum {
   RNNB_EINVAL = 1,       /* bad argument: the reference raises ValueError */
   RNNB_ECUDA = 2,        /* CUDA runtime / launch failure */
   RNNB_ENOMEM = 3,
-  RNNB_EUNSUPPORTED = 4  /* valid request this build does not handle */
+  RNNB_EUNSUPPORTED = 4, /* valid request this build does not handle */
+  RNNB_EFORMAT = 5       /* RNNW/RNNX file error; the message starts with the reference's
+                            exception class (BadMagicError, UnsupportedVersionError,
+                            TruncatedFileError, ShapeConsistencyError; model_io.py:55-72) */
 } rnnb_status;
 
 typedef enum { RNNB_SRU = 1, RNNB_QRNN = 2 } rnnb_cell;
@@ -155,6 +158,21 @@ rnnb_status rnnb_lstm_forward_host(rnnb_lstm_t h, const void* X, int64_t L, int6
 /* what: 0 weight bytes, 1 launches of the last forward, 2 units per CTA,
  * 3 = 1 if the CTA's U rows were shared-memory resident, 4 grid size. */
 rnnb_status rnnb_lstm_query(rnnb_lstm_t h, int what, int64_t* value);
+
+/* ---- RNNW / RNNX files -> device ----
+ * Formats and validation of model_io.py:1-33, 209-308 (sizes checked
+ * against the file before any allocation).  kind codes 0 LSTM, 1 SRU,
+ * 2 QRNN; precision codes 0 f32, 1 f64. */
+rnnb_status rnnb_rnnw_info(const char* path, int* kind, int* precision, int* n_layers, int64_t* d_in,
+                           int64_t* d_h, int max_layers);
+/* load_weights + rnnb_stack_create + rnnb_stack_set_layer for every layer. */
+rnnb_status rnnb_stack_load_rnnw(rnnb_stack_t* out, const char* path, int mode, int device);
+/* One LSTM layer of an RNNW file into an rnnb_lstm handle. */
+rnnb_status rnnb_lstm_load_rnnw(rnnb_lstm_t* out, const char* path, int layer, int mode, int device);
+rnnb_status rnnb_rnnx_info(const char* path, int* precision, int64_t* seq_len, int64_t* width);
+/* load_sequence payload into dst ([seq_len x width], element type dst_dtype),
+ * on the device through a pinned staging ring when dst_on_device. */
+rnnb_status rnnb_rnnx_load(const char* path, void* dst, int dst_dtype, int dst_on_device, void* stream);
 
 /* Introspection for benches/tests. what: 0 = device weight bytes,
  * 1 = kernel launches issued by the last forward, 2 = units per CTA of

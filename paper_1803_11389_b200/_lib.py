@@ -11,7 +11,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RNNB_LIB", os.path.join(HERE, "librnnb.so"))  # override for A/B timing only
 
-OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED = 0, 1, 2, 3, 4
+OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED, EFORMAT = 0, 1, 2, 3, 4, 5
 SRU, QRNN = 1, 2
 MODES = {"f32": 0, "f64": 1, "bf16": 2, "tf32": 3, "f32x3": 4}
 DT_F32, DT_F64 = 0, 1
@@ -22,7 +22,8 @@ SYMBOLS = (
     "rnnb_stack_destroy", "rnnb_stack_set_layer", "rnnb_forward", "rnnb_forward_host",
     "rnnb_gates", "rnnb_sweep", "rnnb_finalize", "rnnb_query", "rnnb_stack_create_ex",
     "rnnb_stack_set_highway", "rnnb_lstm_create", "rnnb_lstm_destroy", "rnnb_lstm_set_weights",
-    "rnnb_lstm_forward", "rnnb_lstm_forward_host", "rnnb_lstm_query",
+    "rnnb_lstm_forward", "rnnb_lstm_forward_host", "rnnb_lstm_query", "rnnb_rnnw_info",
+    "rnnb_stack_load_rnnw", "rnnb_lstm_load_rnnw", "rnnb_rnnx_info", "rnnb_rnnx_load",
 )
 FLAG_WIDE_SRU = 1
 
@@ -65,6 +66,12 @@ def load():
         "rnnb_lstm_forward": ([vp, vp, i64, i64, i64, vp, i64, vp, vp, vp], ci),
         "rnnb_lstm_forward_host": ([vp, vp, i64, i64, vp, vp, vp, vp], ci),
         "rnnb_lstm_query": ([vp, ci, P64], ci),
+        "rnnb_rnnw_info": ([ctypes.c_char_p, ctypes.POINTER(ci), ctypes.POINTER(ci), ctypes.POINTER(ci), P64, P64,
+                            ci], ci),
+        "rnnb_stack_load_rnnw": ([ctypes.POINTER(vp), ctypes.c_char_p, ci, ci], ci),
+        "rnnb_lstm_load_rnnw": ([ctypes.POINTER(vp), ctypes.c_char_p, ci, ci, ci], ci),
+        "rnnb_rnnx_info": ([ctypes.c_char_p, ctypes.POINTER(ci), P64, P64], ci),
+        "rnnb_rnnx_load": ([ctypes.c_char_p, vp, ci, ci, vp], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -79,6 +86,10 @@ def check(status):
     if status == OK:
         return
     msg = load().rnnb_last_error().decode(errors="replace")
+    if status == EFORMAT:
+        from . import model_io
+        cls, _, text = msg.partition(": ")
+        raise getattr(model_io, cls, model_io.FileFormatError)(text or msg)
     if status == EINVAL:
         raise ValueError(msg)
     raise RnnbError(f"rnnb status {status}: {msg}")

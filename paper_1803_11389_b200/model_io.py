@@ -1,0 +1,231 @@
+"""RNNW / RNNX files: the reference's serialisation
+(rnnblock model_io.py:1-33, 190-308) with the same exception classes, plus
+loaders that go from a file straight into the device layouts through the C
+ABI (``rnnb_stack_load_rnnw``, ``rnnb_lstm_load_rnnw``, ``rnnb_rnnx_load``).
+
+Host-side ``save_* / load_*`` produce and accept byte-identical files to the
+reference's (little-endian, fixed headers, row-major, canonical field
+order); the native loaders validate the same way (sizes checked against the
+file before any allocation) and report the reference's exception class.
+"""
+
+import ctypes
+import dataclasses
+import os
+import struct
+
+import numpy as np
+
+from . import _lib
+from .cells import PRECISIONS, CellKind, LstmWeights, QrnnWeights, RnnConfig, SruWeights, WeightSet
+
+_WEIGHT_MAGIC = b"RNNW"
+_SEQ_MAGIC = b"RNNX"
+_VERSION = 1
+_KIND_CODES = {CellKind.LSTM: 0, CellKind.SRU: 1, CellKind.QRNN: 2}
+_KIND_FROM = {v: k for k, v in _KIND_CODES.items()}
+_PREC_CODES = {"f32": 0, "f64": 1}
+_PREC_FROM = {v: k for k, v in _PREC_CODES.items()}
+_LAYER_CLASS = {CellKind.LSTM: LstmWeights, CellKind.SRU: SruWeights, CellKind.QRNN: QrnnWeights}
+
+
+class FileFormatError(ValueError):
+    """Base class of serialisation errors (model_io.py:55)."""
+
+
+class BadMagicError(FileFormatError):
+    pass
+
+
+class UnsupportedVersionError(FileFormatError):
+    pass
+
+
+class TruncatedFileError(FileFormatError):
+    pass
+
+
+class ShapeConsistencyError(FileFormatError):
+    pass
+
+
+def layer_spec(kind, d_in, d_h):
+    """Canonical shapes of one layer (model_io.py:133-139)."""
+    if kind is CellKind.LSTM:
+        return [(d_h, d_in)] * 4 + [(d_h, d_h)] * 4 + [(d_h,)] * 4
+    if kind is CellKind.SRU:
+        return [(d_h, d_in)] * 3 + [(d_h,)] * 2
+    return [(d_h, d_in)] * 6
+
+
+def _dt(precision):
+    return np.dtype("<f4") if precision == "f32" else np.dtype("<f8")
+
+
+def save_weights(ws: WeightSet, path) -> None:
+    with open(path, "wb") as f:
+        f.write(struct.pack("<4sIBBHI", _WEIGHT_MAGIC, _VERSION, _KIND_CODES[ws.kind], _PREC_CODES[ws.precision],
+                            0, len(ws.layers)))
+        dt = _dt(ws.precision)
+        for layer in ws.layers:
+            f.write(struct.pack("<II", layer.d_in, layer.d_h))
+            for fld in dataclasses.fields(layer):
+                f.write(np.ascontiguousarray(getattr(layer, fld.name), dtype=dt).tobytes())
+
+
+def _read(f, n, what):
+    buf = f.read(n)
+    if len(buf) != n:
+        raise TruncatedFileError(f"file ends inside {what} ({len(buf)} of {n} bytes)")
+    return buf
+
+
+def _remaining(f):
+    pos = f.tell()
+    end = f.seek(0, 2)
+    f.seek(pos)
+    return end - pos
+
+
+def load_weights(path) -> WeightSet:
+    with open(path, "rb") as f:
+        magic, version, kc, pc, _, n_layers = struct.unpack("<4sIBBHI", _read(f, 16, "header"))
+        if magic != _WEIGHT_MAGIC:
+            raise BadMagicError(f"bad magic {magic!r}, expected {_WEIGHT_MAGIC!r}")
+        if version != _VERSION:
+            raise UnsupportedVersionError(f"format version {version}, expected {_VERSION}")
+        if kc not in _KIND_FROM:
+            raise ShapeConsistencyError(f"unknown cell kind code {kc}")
+        if pc not in _PREC_FROM:
+            raise ShapeConsistencyError(f"unknown precision code {pc}")
+        if n_layers < 1:
+            raise ShapeConsistencyError("layer count must be >= 1")
+        kind, precision = _KIND_FROM[kc], _PREC_FROM[pc]
+        dt = _dt(precision)
+        layers, prev = [], None
+        for li in range(n_layers):
+            d_in, d_h = struct.unpack("<II", _read(f, 8, f"layer {li} header"))
+            if d_in < 1 or d_h < 1:
+                raise ShapeConsistencyError(f"layer {li} has zero dimension")
+            if kind is CellKind.SRU and d_in != d_h:
+                raise ShapeConsistencyError("SRU layer must have d_in == d_h")
+            if prev is not None and d_in != prev:
+                raise ShapeConsistencyError(f"layer {li} input width {d_in} does not match previous layer "
+                                            f"width {prev}")
+            prev = d_h
+            spec = layer_spec(kind, d_in, d_h)
+            if _remaining(f) < sum(int(np.prod(s)) for s in spec) * dt.itemsize:
+                raise TruncatedFileError(f"layer {li} payload incomplete")
+            arrays = []
+            for shape in spec:
+                n = int(np.prod(shape))
+                buf = _read(f, n * dt.itemsize, f"layer {li} data")
+                arrays.append(np.frombuffer(buf, dtype=dt).astype(PRECISIONS[precision]).reshape(shape).copy())
+            layers.append(_LAYER_CLASS[kind](*arrays))
+        if f.read(1):
+            raise ShapeConsistencyError("trailing bytes after final layer")
+    return WeightSet(kind=kind, precision=precision, layers=layers)
+
+
+def save_sequence(X: np.ndarray, path) -> None:
+    if X.ndim != 2:
+        raise ValueError("sequence must be a 2-d array")
+    if X.dtype not in (np.float32, np.float64):
+        raise ValueError(f"unsupported dtype {X.dtype}")
+    precision = "f32" if X.dtype == np.float32 else "f64"
+    with open(path, "wb") as f:
+        f.write(struct.pack("<4sIBBHII", _SEQ_MAGIC, _VERSION, _PREC_CODES[precision], 0, 0, X.shape[0], X.shape[1]))
+        f.write(np.ascontiguousarray(X, dtype=_dt(precision)).tobytes())
+
+
+def load_sequence(path) -> np.ndarray:
+    with open(path, "rb") as f:
+        magic, version, pc, _, _, seq_len, width = struct.unpack("<4sIBBHII", _read(f, 20, "header"))
+        if magic != _SEQ_MAGIC:
+            raise BadMagicError(f"bad magic {magic!r}, expected {_SEQ_MAGIC!r}")
+        if version != _VERSION:
+            raise UnsupportedVersionError(f"format version {version}, expected {_VERSION}")
+        if pc not in _PREC_FROM:
+            raise ShapeConsistencyError(f"unknown precision code {pc}")
+        if seq_len < 1 or width < 1:
+            raise ShapeConsistencyError("sequence dimensions must be >= 1")
+        precision = _PREC_FROM[pc]
+        dt = _dt(precision)
+        payload = seq_len * width * dt.itemsize
+        got = _remaining(f)
+        if got < payload:
+            raise TruncatedFileError(f"payload incomplete ({got} of {payload} bytes)")
+        if got > payload:
+            raise ShapeConsistencyError("trailing bytes after payload")
+        buf = _read(f, payload, "payload")
+    return np.frombuffer(buf, dtype=dt).astype(PRECISIONS[precision]).reshape(seq_len, width).copy()
+
+
+# ---------------------------------------------------------------------------
+# native: file -> device
+
+
+def _path(p):
+    return os.fsencode(os.fspath(p))
+
+
+def weights_info(path):
+    """(kind, precision, [(d_in, d_h), ...]) of an RNNW file, validated natively."""
+    lib = _lib.load()
+    k, p, n = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    _lib.check(lib.rnnb_rnnw_info(_path(path), ctypes.byref(k), ctypes.byref(p), ctypes.byref(n), None, None, 0))
+    din = (ctypes.c_int64 * n.value)()
+    dh = (ctypes.c_int64 * n.value)()
+    _lib.check(lib.rnnb_rnnw_info(_path(path), ctypes.byref(k), ctypes.byref(p), ctypes.byref(n), din, dh, n.value))
+    return _KIND_FROM[k.value], _PREC_FROM[p.value], list(zip(list(din), list(dh)))
+
+
+def sequence_info(path):
+    lib = _lib.load()
+    p, L, W = ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
+    _lib.check(lib.rnnb_rnnx_info(_path(path), ctypes.byref(p), ctypes.byref(L), ctypes.byref(W)))
+    return _PREC_FROM[p.value], L.value, W.value
+
+
+def load_weights_device(path, mode=None, device=None, layer=0):
+    """An RNNW file straight into a device handle: ``DeviceStack`` for
+    SRU/QRNN, ``DeviceLstm`` (layer ``layer``) for LSTM.  mode defaults to
+    the file's precision."""
+    import torch
+
+    from .device import DeviceLstm, DeviceStack
+    kind, precision, dims = weights_info(path)
+    mode = mode or precision
+    dev = torch.cuda.current_device() if device is None else int(device)
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+    if kind is CellKind.LSTM:
+        _lib.check(lib.rnnb_lstm_load_rnnw(ctypes.byref(h), _path(path), int(layer), _lib.MODES[mode], dev))
+        obj = DeviceLstm.__new__(DeviceLstm)
+        obj.lib, obj.mode, obj.device, obj._h = lib, mode, dev, h
+        obj.d_in, obj.d_h = dims[layer]
+        return obj
+    _lib.check(lib.rnnb_stack_load_rnnw(ctypes.byref(h), _path(path), _lib.MODES[mode], dev))
+    obj = DeviceStack.__new__(DeviceStack)
+    obj.lib, obj.kind, obj.mode, obj.device, obj._h = lib, _KIND_CODES[kind], mode, dev, h
+    obj.d_in = [d[0] for d in dims]
+    obj.d_h = [d[1] for d in dims]
+    return obj
+
+
+def load_sequence_device(path, dtype=None, device=None, stream=None):
+    """An RNNX payload into a new CUDA tensor (pinned staging, async H2D)."""
+    import torch
+
+    from .device import _stream_ptr
+    precision, L, W = sequence_info(path)
+    dtype = dtype or (torch.float64 if precision == "f64" else torch.float32)
+    out = torch.empty((L, W), dtype=dtype, device=device if device is not None else "cuda")
+    dt = _lib.DT_F64 if dtype == torch.float64 else _lib.DT_F32
+    _lib.check(_lib.load().rnnb_rnnx_load(_path(path), ctypes.c_void_p(out.data_ptr()), dt, 1, _stream_ptr(stream)))
+    return out
+
+
+def config_of(ws: WeightSet) -> RnnConfig:
+    first = ws.layers[0]
+    return RnnConfig(ws.kind, first.d_in, first.d_h, n_layers=len(ws.layers), precision=ws.precision)

@@ -236,8 +236,26 @@ def baseline_cfgs():
     np.savez_compressed(os.path.join(HERE, "baseline_cfg.npz"), **out)
 
 
+def model_files():
+    """Reference-written RNNW / RNNX files (model_io.save_weights /
+    save_sequence) for the file-format tests."""
+    from rnnblock import model_io as rbm
+    specs = [("sru2_f32.rnnw", "sru", 24, 24, 2, "f32", 31), ("qrnn1_f64.rnnw", "qrnn", 20, 12, 1, "f64", 32),
+             ("lstm1_f32.rnnw", "lstm", 10, 14, 1, "f32", 33)]
+    index = {}
+    for name, kind, din, dh, nl, prec, seed in specs:
+        cfg = rb.RnnConfig(rbc.CellKind.parse(kind), din, dh, n_layers=nl, precision=prec)
+        rbm.save_weights(rb.generate_weights(cfg, seed), os.path.join(HERE, name))
+        index[name] = {"kind": kind, "d_in": din, "d_h": dh, "n_layers": nl, "precision": prec, "seed": seed}
+    for name, L, W, prec, seed in (("seq_f32.rnnx", 37, 24, "f32", 34), ("seq_f64.rnnx", 11, 20, "f64", 35)):
+        rbm.save_sequence(rb.generate_sequence(L, W, seed, prec), os.path.join(HERE, name))
+        index[name] = {"seq_len": L, "width": W, "precision": prec, "seed": seed}
+    with open(os.path.join(HERE, "model_files.json"), "w") as f:
+        json.dump(index, f, indent=1)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases"]
+    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases", "model_files"]
     for part in parts:
         globals()[part]()
     print("golden fixtures written to", HERE, parts)
