@@ -254,8 +254,30 @@ def model_files():
         json.dump(index, f, indent=1)
 
 
+def traffic():
+    """estimate_traffic / expected_phase_touches / lstm_split_bytes of the
+    reference's traffic model for a grid of configs."""
+    from rnnblock import traffic as rbt
+    out = []
+    for kind, din, dh, nl, prec in (("sru", 512, 512, 1, "f32"), ("qrnn", 1024, 1024, 1, "f32"),
+                                    ("lstm", 350, 350, 2, "f32"), ("qrnn", 300, 200, 3, "f64"),
+                                    ("lstm", 64, 96, 1, "f64")):
+        cfg = rb.RnnConfig(rbc.CellKind.parse(kind), din, dh, n_layers=nl, precision=prec)
+        for L, T in ((2048, 1), (2048, 32), (1000, 7), (5, 64)):
+            r = rbt.estimate_traffic(cfg, L, T)
+            row = {"kind": kind, "d_in": din, "d_h": dh, "n_layers": nl, "precision": prec, "L": L, "T": T,
+                   "weight_bytes": r.weight_bytes, "blocks": r.blocks, "est": r.est_weight_traffic,
+                   "per_step": r.per_step_traffic, "ratio": r.ratio_vs_t1,
+                   "touches": rbt.expected_phase_touches(cfg, L, T)}
+            if kind == "lstm":
+                row["split"] = list(rbt.lstm_split_bytes(cfg))
+            out.append(row)
+    with open(os.path.join(HERE, "traffic.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases", "model_files"]
+    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases", "model_files", "traffic"]
     for part in parts:
         globals()[part]()
     print("golden fixtures written to", HERE, parts)
