@@ -276,8 +276,23 @@ def traffic():
         json.dump(out, f, indent=1)
 
 
+def bench_csv():
+    """emit_csv of fixed rows by the reference (bench.py:194-229)."""
+    import importlib
+    rbbench = importlib.import_module("rnnblock.bench")
+    from rnnblock import traffic as rbt
+    recs = [rbbench.BenchRecord("qrnn", "blocked", 16, 16, 64, T, 8, r, 10.0 / T + 0.25 * r)
+            for T in (1, 4) for r in range(3)]
+    rbbench.emit_csv(recs, os.path.join(HERE, "bench_records.csv"), kind="records")
+    rows = rbbench.summarize(recs) + [rbbench.SpeedupRow("LSTM", 673.667, None)]
+    rbbench.emit_csv(rows, os.path.join(HERE, "bench_summary.csv"), kind="summary")
+    cfg = rb.RnnConfig(rbc.CellKind.QRNN, 64, 64, precision="f32")
+    rbbench.emit_csv([rbt.estimate_traffic(cfg, 100, T) for T in (1, 8)], os.path.join(HERE, "bench_traffic.csv"),
+                     kind="traffic")
+
+
 if __name__ == "__main__":
-    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases", "model_files", "traffic"]
+    parts = sys.argv[1:] or ["cells_d2", "splitmix", "blocked_cases", "baseline_cfgs", "lstm_cases", "model_files", "traffic", "bench_csv"]
     for part in parts:
         globals()[part]()
     print("golden fixtures written to", HERE, parts)
