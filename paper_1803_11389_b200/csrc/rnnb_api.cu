@@ -664,9 +664,14 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
       !g_stream_disabled && !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
   StreamOps so = stream_ops();
   if (want_stream && so.write && so.wait) {
-    // chunk: whole blocks, >= 128 steps, at most kMaxStreamChunks of them
+    // chunk: whole blocks, >= kMinChunk steps (RNNB_STREAM_CHUNK), at most
+    // kMaxStreamChunks of them; small chunks shorten the exposed first
+    // copy-in and last copy-out
+    const char* env_c = getenv("RNNB_STREAM_CHUNK");
+    const int64_t min_chunk = env_c ? atoll(env_c) : 64;  // measured cfg2: 32 -> 2.11M, 64 -> 2.60M, 128 -> 2.57M, 256 -> 2.51M e2e
     int64_t sc = (L + kMaxStreamChunks - 1) / kMaxStreamChunks;
-    if (sc < 128) sc = 128;
+    if (sc < min_chunk) sc = min_chunk;
+    if (sc < 1) sc = 1;
     sc = (sc + T - 1) / T * T;
     const int64_t nsc = (L + sc - 1) / sc;
     if (nsc <= kMaxStreamChunks) {
