@@ -333,7 +333,7 @@ def run_ours(args, rank, world, local_rank):
         "modes": {m: sweep_of(r, m) for m, r in extra.items()},
         "clocks": head["clocks"],
     }
-    if args.cpu_baseline:
+    if args.cpu_baseline and world == 1:  # the CPU baseline is a rank-0, N=1 measurement
         line["cpu_baseline"] = cpu_baseline(args, w, sample_steps=args.cpu_sample)
     st.close()
     return line
@@ -425,6 +425,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # BENCH_DIST_BACKEND=gloo + BENCH_SHARE_GPU=1: exercise the N>1 code path
+    # with independent replicas sharing one GPU (host-logic check only; the
+    # driver's scaling runs use nccl, one GPU per rank)
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    if os.environ.get("BENCH_SHARE_GPU") == "1":
+        local_rank = 0
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
@@ -432,7 +438,10 @@ def main():
             import torch
             import torch.distributed as dist
             torch.cuda.set_device(local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            else:
+                dist.init_process_group(backend)
         line = run_ours(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
