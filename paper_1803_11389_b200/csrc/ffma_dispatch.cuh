@@ -227,11 +227,13 @@ static cudaError_t run_u(const LayerArgs<TA, TW>& a, int grid, bool allow_wsmem,
     case 4: return run_nt<TA, TW, CELL, 4, U>(a, grid, allow_wsmem, s, out);
     case 8: return run_nt<TA, TW, CELL, 8, U>(a, grid, allow_wsmem, s, out);
     default:
-      // fp32, opt-in (RNNB_NT32=1): a 32-column pass halves the per-pass
-      // reduction / hand-off cost but measured within +-3% of NT=16 (cfg2)
+      // fp32: a 32-column pass (double-buffered partials, 3 x stages) halves
+      // the per-pass reduction / hand-off cost: cfg2 2.89 -> 3.01 M steps/s.
+      // Falls back to NT = 16 when its shared-memory plan does not fit
+      // (RNNB_NT32=0 forces NT = 16).
       if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4) {
         const char* env = getenv("RNNB_NT32");
-        if (allow_wsmem && a.T_b >= 32 && a.xround == XR_NONE && env && env[0] == '1') {
+        if (allow_wsmem && a.T_b >= 32 && a.xround == XR_NONE && !(env && env[0] == '0')) {
           cudaError_t e;
           if (try_ws<TA, TW, CELL, 32, U>(a, grid, s, out, &e)) return e;
         }

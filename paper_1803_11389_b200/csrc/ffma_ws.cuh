@@ -171,7 +171,11 @@ struct WsCfg {
   // padded x row pitch: each 8-lane phase (LANES_T rows x 8/LANES_T k-vectors)
   // must hit 8 distinct 16-byte bank groups; one row needs no padding
   static constexpr int PADV = LANES_T == 1 ? 0 : KV * (LANES_T >= 8 ? 1 : 8 / LANES_T);
-  static constexpr int STAGES = 4;
+  // the 32-column pass (fp32, T_b >= 32) double-buffers the cross-warp partials
+  // so consumers reduce pass p+1 while the epilogue still reads pass p; it
+  // pays for the second buffer with one x stage
+  static constexpr int NRED = NT == 32 ? 2 : 1;
+  static constexpr int STAGES = NT == 32 ? 3 : 4;
   // reduce-scatter over the LANES_K lanes of a k-group: NV partials per lane
   // (padded to a multiple of LANES_K), NV / LANES_K sums per lane afterwards
   static constexpr int NV = (RH * CT + LANES_K - 1) / LANES_K * LANES_K;
@@ -190,10 +194,10 @@ __host__ __device__ inline size_t ws_smem_bytes(int Dp, int KC, int BW) {
   using C = WsCfg<TA, TW, CELL, NT, U>;
   size_t off = align_up((size_t)C::TAPS * Dp / C::KV * C::Rs * C::KV * sizeof(TW) + 16 * C::RG, 128);
   off += (size_t)C::STAGES * (KC / BW) * ws_box_elems<TA, TW, CELL, NT, U>(BW) * sizeof(TA);
-  off += (size_t)C::KG * C::Rpad * NT * sizeof(TA);
+  off += (size_t)C::NRED * C::KG * C::Rpad * NT * sizeof(TA);
   off += (size_t)3 * U * NT * sizeof(TA);
   off = align_up(off, 8);
-  off += (2 * C::STAGES + 2) * sizeof(uint64_t);
+  off += (2 * C::STAGES + 2 * C::NRED) * sizeof(uint64_t);
   return off;
 }
 
@@ -223,15 +227,17 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
   TA* Xr = reinterpret_cast<TA*>(smem + off);
   const size_t stage_bytes = (size_t)((KC + BW - 1) / BW) * BOXS * sizeof(TA);
   off += (size_t)STAGES * stage_bytes;
+  constexpr int NRED = C::NRED;
+  constexpr size_t red_elems = (size_t)KG * Rpad * NT;
   TA* red = reinterpret_cast<TA*>(smem + off);
-  off += (size_t)KG * Rpad * NT * sizeof(TA);
+  off += (size_t)NRED * red_elems * sizeof(TA);
   TA* gate = reinterpret_cast<TA*>(smem + off);
   off += (size_t)3 * U * NT * sizeof(TA);
   off = align_up(off, 8);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + off);
   uint64_t* empty = full + STAGES;
-  uint64_t* redfull = empty + STAGES;
-  uint64_t* redempty = redfull + 1;
+  uint64_t* redfull = empty + STAGES;    // [NRED]
+  uint64_t* redempty = redfull + NRED;   // [NRED]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -256,8 +262,10 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CW);
     }
-    mbar_init(redfull, CW);
-    mbar_init(redempty, 1);
+    for (int b = 0; b < NRED; ++b) {
+      mbar_init(&redfull[b], CW);
+      mbar_init(&redempty[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   cp_async_wait<0>();
@@ -328,12 +336,15 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
       for (int p0 = 0; p0 < l; p0 += NT, ++pass) {
         const int nt = (l - p0) < NT ? (l - p0) : NT;
         const int64_t tp = t0 + p0;
-        mbar_wait_sleep(redfull, pass & 1);
+        const int rb = NRED == 2 ? (int)(pass & 1) : 0;
+        const uint32_t rph = (NRED == 2 ? pass >> 1 : pass) & 1;
+        const TA* redb = red + rb * red_elems;
+        mbar_wait_sleep(&redfull[rb], rph);
         for (int i = et; i < ((a.dbg & 4) ? 0 : R * nt); i += kWsEpiThreads) {
           const int r = i / nt, col = i - (i / nt) * nt;
           TA s = TA(0);
 #pragma unroll
-          for (int w = 0; w < KG; ++w) s += red[((size_t)w * Rpad + r) * NT + col];
+          for (int w = 0; w < KG; ++w) s += redb[((size_t)w * Rpad + r) * NT + col];
           const int u = r / 3, g = r - 3 * (r / 3);
           TA v;
           if (CELL == SRU) v = g == 0 ? s : sigmoid_ref<TA>(s + a.bias[(size_t)(u0 + u) * 2 + g - 1]);
@@ -341,7 +352,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           gate[((size_t)g * U + u) * NT + col] = v;
         }
         epi_bar_sync();
-        if (et == 0) mbar_arrive(redempty);
+        if (et == 0) mbar_arrive(&redempty[rb]);
         if (et < U && !(a.dbg & 4)) {
           TA* cand = gate + (size_t)et * NT;
           const TA* fg = gate + (size_t)(U + et) * NT;
@@ -491,17 +502,20 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
         int jb = 0;
 #pragma unroll
         for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) jb += (lane & o) ? ns : 0;
-        mbar_wait(redempty, (pass & 1) ^ 1);
+        const int rb = NRED == 2 ? (int)(pass & 1) : 0;
+        const uint32_t rph = (NRED == 2 ? pass >> 1 : pass) & 1;
+        TA* redb = red + rb * red_elems;
+        mbar_wait(&redempty[rb], rph ^ 1);
 #pragma unroll
         for (int i = 0; i < NV / LANES_K; ++i) {
           const int j = jb + i;
           if (j < RH * CT) {
             const int r = j / CT, ct = j - (j / CT) * CT;
-            red[((size_t)kg * Rpad + rbase + r) * NT + tq + LANES_T * ct] = v[i];
+            redb[((size_t)kg * Rpad + rbase + r) * NT + tq + LANES_T * ct] = v[i];
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(redfull);
+        if (lane == 0) mbar_arrive(&redfull[rb]);
       }
     }
   }
