@@ -59,7 +59,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 // off-critical-path wait (producer / epilogue): back off with nanosleep so the
 // spinning warp does not steal issue slots from the FFMA consumers
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t max_ns = 1024) {
   uint32_t ns = 32;
   while (true) {
     uint32_t ok;
@@ -72,7 +72,7 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
         : "memory");
     if (ok) return;
     __nanosleep(ns);
-    ns = ns < 1024 ? ns * 2 : 1024;
+    ns = ns < max_ns ? ns * 2 : max_ns;
   }
 }
 // 2-D TMA tile load (tensor map in param space), completion on `bar`
@@ -174,7 +174,9 @@ struct WsCfg {
   // the 32-column pass (fp32, T_b >= 32) double-buffers the cross-warp partials
   // so consumers reduce pass p+1 while the epilogue still reads pass p; it
   // pays for the second buffer with one x stage
-  static constexpr int NRED = NT == 32 ? 2 : 1;
+  // (also the short fp32 passes, NT <= 8, where a pass lasts ~1 us and the
+  // buffers cost < 3 KB)
+  static constexpr int NRED = (NT == 32 || (sizeof(TA) == 4 && NT <= 8)) ? 2 : 1;
   static constexpr int STAGES = NT == 32 ? 3 : 4;
   // reduce-scatter over the LANES_K lanes of a k-group: NV partials per lane
   // (padded to a multiple of LANES_K), NV / LANES_K sums per lane afterwards
@@ -339,7 +341,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
         const int rb = NRED == 2 ? (int)(pass & 1) : 0;
         const uint32_t rph = (NRED == 2 ? pass >> 1 : pass) & 1;
         const TA* redb = red + rb * red_elems;
-        mbar_wait_sleep(&redfull[rb], rph);
+        mbar_wait_sleep(&redfull[rb], rph, NT <= 8 ? 128u : 1024u);  // short passes: wake promptly
         for (int i = et; i < ((a.dbg & 4) ? 0 : R * nt); i += kWsEpiThreads) {
           const int r = i / nt, col = i - (i / nt) * nt;
           TA s = TA(0);
