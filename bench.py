@@ -209,6 +209,10 @@ def time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_
             ev[i][0].record(stream)
             st.forward(X, T_b, out=out)
             ev[i][1].record(stream)
+        if sampler is not None:
+            # poll (GIL released between polls) so the sampler thread runs while the GPU works
+            while not ev[-1][1].query():
+                time.sleep(0.0005)
         torch.cuda.synchronize()
         if dist:
             torch.distributed.barrier()

@@ -668,7 +668,7 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
     // kMaxStreamChunks of them; small chunks shorten the exposed first
     // copy-in and last copy-out
     const char* env_c = getenv("RNNB_STREAM_CHUNK");
-    const int64_t min_chunk = env_c ? atoll(env_c) : 64;  // measured cfg2: 32 -> 2.11M, 64 -> 2.60M, 128 -> 2.57M, 256 -> 2.51M e2e
+    const int64_t min_chunk = env_c ? atoll(env_c) : 128;  // measured cfg2 (32-column passes): 64 -> 2.17-2.42M (noisy), 128 -> 2.64M, 256 -> 2.56M e2e
     int64_t sc = (L + kMaxStreamChunks - 1) / kMaxStreamChunks;
     if (sc < min_chunk) sc = min_chunk;
     if (sc < 1) sc = 1;

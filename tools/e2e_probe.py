@@ -1,0 +1,39 @@
+"""Wall-clock timing of the host-buffer entry point (rnnb_forward_host) for
+one workload, as bench.py's e2e leg measures it; for tuning the streaming
+path (RNNB_STREAM_CHUNK, RNNB_NT32, RNNB_HOST_STREAM).  Not the bench."""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1803_11389_b200 as P  # noqa: E402
+from paper_1803_11389_b200 import workloads  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--workload", default="cfg2")
+ap.add_argument("--block", type=int, default=32)
+ap.add_argument("--mode", default="f32")
+ap.add_argument("--reps", type=int, default=50)
+ap.add_argument("--tag", default="")
+a = ap.parse_args()
+w = workloads.make(a.workload)
+st = P.DeviceStack(w.kind, w.layers, mode=a.mode)
+Xh = torch.from_numpy(w.X.astype(st.np_dtype)).pin_memory()
+Hh = torch.empty((w.seq_len, st.d_h[-1]), dtype=st.dtype).pin_memory()
+Xn, Hn = Xh.numpy(), Hh.numpy()
+for _ in range(5):
+    st.forward_host(Xn, a.block, out=Hn)
+torch.cuda.synchronize()
+ts = []
+for _ in range(a.reps):
+    t0 = time.perf_counter()
+    st.forward_host(Xn, a.block, out=Hn)
+    ts.append(time.perf_counter() - t0)
+ts = np.array(ts) * 1e3
+L = w.seq_len
+print(f"{a.tag} {a.workload} {a.mode} T_b={a.block}: mean {ts.mean():.4f} ms ({L / ts.mean() * 1e-3:.3f} M steps/s) "
+      f"median {np.median(ts):.4f} min {ts.min():.4f} max {ts.max():.4f}", flush=True)
