@@ -174,6 +174,42 @@ rnnb_status rnnb_rnnx_info(const char* path, int* precision, int64_t* seq_len, i
  * on the device through a pinned staging ring when dst_on_device. */
 rnnb_status rnnb_rnnx_load(const char* path, void* dst, int dst_dtype, int dst_on_device, void* stream);
 
+/* ---- Multi-GPU partitions: fused peer-memory hand-off ----
+ * The reference has no distributed path; these replace the
+ * NCCL send/recv / all-gather between launches (paper_1803_11389_b200/
+ * partition.py) with stores from the layer epilogue straight into the
+ * consumer GPU's buffer over NVLink, plus stream-ordered flags.
+ *
+ * rnnb_forward_ex: rnnb_forward whose LAST layer also stores every h value
+ * to n_peers (<= RNNB_MAX_PEERS) extra destinations with H's layout (mapped
+ * peer buffers: the next pipeline stage's input ring, or every rank's
+ * all-gathered next-layer input).  ldh may be negative (|ldh| >= d_h): rows
+ * are then stored in reverse time order (the backward direction of a
+ * bidirectional layer writes its reversed output in place). */
+#define RNNB_MAX_PEERS 7
+rnnb_status rnnb_forward_ex(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size,
+                            void* H, int64_t ldh, void* c_state, void* x_carry, int n_peers,
+                            void* const* peer_H, void* stream);
+/* Zeroed device allocation of its own (cudaMalloc). */
+rnnb_status rnnb_dev_alloc(int device, size_t bytes, void** ptr);
+rnnb_status rnnb_dev_free(int device, void* ptr);
+/* CUDA IPC export / import (one process per GPU).  handle names the whole
+ * device allocation holding ptr (any cudaMalloc-backed pointer, e.g. a
+ * caching-allocator tensor); *offset = ptr's byte offset inside it, so the
+ * importer's address is rnnb_ipc_open's base + offset. */
+#define RNNB_IPC_HANDLE_BYTES 64
+rnnb_status rnnb_ipc_handle(const void* ptr, void* handle, uint64_t* offset);
+rnnb_status rnnb_ipc_open(int device, const void* handle, void** base);
+rnnb_status rnnb_ipc_close(int device, void* ptr);
+/* Direct peer loads/stores between two devices of one process. */
+rnnb_status rnnb_peer_access(int device, int peer);
+/* Stream-ordered flags (32-bit, compared as wrapping GEQ).  signal: after all
+ * earlier work of `stream`, *flag = value with system-scope release (flag may
+ * be a mapped peer address).  wait: later work of `stream` starts once
+ * *flag >= value (a stream wait operation; no kernel spins). */
+rnnb_status rnnb_flag_signal(int device, void* flag, uint32_t value, void* stream);
+rnnb_status rnnb_flag_wait(int device, const void* flag, uint32_t value, void* stream);
+
 /* Introspection for benches/tests. what: 0 = device weight bytes,
  * 1 = kernel launches issued by the last forward, 2 = units per CTA of
  * `layer`, 3 = 1 if the last forward kept `layer`'s weights resident in

@@ -24,7 +24,11 @@ SYMBOLS = (
     "rnnb_stack_set_highway", "rnnb_lstm_create", "rnnb_lstm_destroy", "rnnb_lstm_set_weights",
     "rnnb_lstm_forward", "rnnb_lstm_forward_host", "rnnb_lstm_query", "rnnb_rnnw_info",
     "rnnb_stack_load_rnnw", "rnnb_lstm_load_rnnw", "rnnb_rnnx_info", "rnnb_rnnx_load",
+    "rnnb_forward_ex", "rnnb_dev_alloc", "rnnb_dev_free", "rnnb_ipc_handle", "rnnb_ipc_open",
+    "rnnb_ipc_close", "rnnb_peer_access", "rnnb_flag_signal", "rnnb_flag_wait",
 )
+MAX_PEERS = 7
+IPC_HANDLE_BYTES = 64
 FLAG_WIDE_SRU = 1
 
 _lib = None
@@ -72,6 +76,15 @@ def load():
         "rnnb_lstm_load_rnnw": ([ctypes.POINTER(vp), ctypes.c_char_p, ci, ci, ci], ci),
         "rnnb_rnnx_info": ([ctypes.c_char_p, ctypes.POINTER(ci), P64, P64], ci),
         "rnnb_rnnx_load": ([ctypes.c_char_p, vp, ci, ci, vp], ci),
+        "rnnb_forward_ex": ([vp, vp, i64, i64, i64, vp, i64, vp, vp, ci, ctypes.POINTER(vp), vp], ci),
+        "rnnb_dev_alloc": ([ci, ctypes.c_size_t, ctypes.POINTER(vp)], ci),
+        "rnnb_dev_free": ([ci, vp], ci),
+        "rnnb_ipc_handle": ([vp, ctypes.c_char_p, ctypes.POINTER(ctypes.c_uint64)], ci),
+        "rnnb_ipc_open": ([ci, ctypes.c_char_p, ctypes.POINTER(vp)], ci),
+        "rnnb_ipc_close": ([ci, vp], ci),
+        "rnnb_peer_access": ([ci, ci], ci),
+        "rnnb_flag_signal": ([ci, vp, ctypes.c_uint32, vp], ci),
+        "rnnb_flag_wait": ([ci, vp, ctypes.c_uint32, vp], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

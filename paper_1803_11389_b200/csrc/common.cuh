@@ -11,6 +11,19 @@
 namespace rnnb {
 
 enum Cell : int { SRU = 1, QRNN = 2 };
+// Extra destinations of the last layer's h stores (peer GPUs' mapped buffers:
+// the pipeline hand-off / all-gather rides on the epilogue's stores).
+constexpr int kMaxPeers = 7;
+
+// h store of a layer epilogue: the local output plus each peer destination
+// (constant indices: no dynamic indexing into the kernel parameter block).
+template <typename Args, typename T>
+__device__ __forceinline__ void store_h(const Args& a, int64_t i, T h) {
+  a.Hout[i] = h;
+#pragma unroll
+  for (int p = 0; p < kMaxPeers; ++p)
+    if (p < a.npeer) a.Hpeer[p][i] = h;
+}
 // x-operand rounding applied inside the FFMA kernel so its numerics match the
 // tensor-core modes (TF32: cvt.rna.tf32; BF16: round-to-nearest-even).
 enum XRound : int { XR_NONE = 0, XR_BF16 = 1, XR_TF32 = 2 };

@@ -39,7 +39,9 @@ struct LayerArgs {
   const TA* Xhw;       // SRU highway source, normally == X
   int64_t ldhw;
   TA* Hout;            // [L][ldh]
-  int64_t ldh;
+  int64_t ldh;         // may be negative (rows stored in reverse time order)
+  TA* Hpeer[kMaxPeers];  // same layout as Hout on peer GPUs (mapped), npeer used
+  int npeer;
   const TA* c_in;      // [H] initial c (nullptr: zeros)
   TA* c_out;           // [H] final c (nullptr: not written)
   TA* G;               // gates-out mode: [3][H][ldg] activated gates, no scan
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffma_layer_kernel(LayerArgs<TA, T
           const TA o = gate[((size_t)2 * U + u) * NT + col];
           TA h = o * tanh_full(c);
           if (CELL == SRU) h = h + (TA(1) - o) * a.Xhw[(tp + col) * a.ldhw + unit];
-          a.Hout[(tp + col) * a.ldh + unit] = h;
+          store_h(a, (tp + col) * a.ldh + unit, h);
         }
       }
     }

@@ -144,7 +144,7 @@ __global__ void __maxnreg__(U == 7 ? 160 : 96) ffma_reg_kernel(LayerArgs<float, 
         c = f * c + (1.f - f) * z;
         float h = o * tanh_full(c);
         if (CELL == SRU) h = h + (1.f - o) * a.Xhw[t * a.ldhw + u0 + lane];
-        a.Hout[t * a.ldh + u0 + lane] = h;
+        store_h(a, t * a.ldh + u0 + lane, h);
       }
     }
     if (lane < U && a.c_out != nullptr && u0 + lane < a.H) a.c_out[u0 + lane] = c;

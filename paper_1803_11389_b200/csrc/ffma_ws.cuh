@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
             const TA o = gate[((size_t)2 * U + u) * NT + col];
             TA h = o * tanh_full(cc);
             if (CELL == SRU) h = h + (TA(1) - o) * a.Xhw[(tp + col) * a.ldhw + unit];
-            a.Hout[(tp + col) * a.ldh + unit] = h;
+            store_h(a, (tp + col) * a.ldh + unit, h);
           }
         }
         epi_bar_sync();

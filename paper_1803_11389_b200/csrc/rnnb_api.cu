@@ -90,6 +90,10 @@ struct rnnb_stack {
   int* stream_done = nullptr;
   int stream_chunk = 0;
   bool stream_refused = false;
+  // rnnb_forward_ex: extra h destinations of the LAST layer (peer GPUs'
+  // mapped buffers); cur_peers is non-zero only while that layer launches
+  int n_peers = 0, cur_peers = 0;
+  void* peer_H[kMaxPeers] = {};
 };
 
 namespace {
@@ -179,6 +183,8 @@ LayerArgs<TA, TW> make_args(const rnnb_stack* h, const Layer& ly) {
   a.h_done = h->stream_done;
   a.stream_fail = h->stream_ready ? h->stream_ctr + 1 : nullptr;
   a.h_chunk = h->stream_chunk;
+  a.npeer = h->cur_peers;
+  for (int p = 0; p < h->cur_peers; ++p) a.Hpeer[p] = static_cast<TA*>(h->peer_H[p]);
   return a;
 }
 
@@ -239,6 +245,8 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.Hout = Hout;
   a.ldh = ldh;
   a.Hop = nullptr;
+  a.npeer = h->cur_peers;
+  for (int p = 0; p < h->cur_peers; ++p) a.Hpeer[p] = static_cast<float*>(h->peer_H[p]);
   a.bias = ly.bias_tc;
   a.cbuf = h->cbuf;
   a.aggA = aggA;
@@ -327,7 +335,9 @@ rnnb_status forward_t(rnnb_stack* h, const TA* X, int64_t ldx, int64_t L, int64_
     const int64_t ldo = last ? ldh : ly.dh;
     TA* c_io = c_state ? c_state + coff : nullptr;
     TA* xc_io = x_carry ? x_carry + xoff : nullptr;
+    h->cur_peers = last ? h->n_peers : 0;
     rnnb_status st = layer_launch<TA, TW>(h, li, in, ldin, L, Tb, out, ldo, c_io, xc_io, nullptr, 0, s);
+    h->cur_peers = 0;
     if (st != RNNB_OK) return st;
     if (xc_io && h->kind == RNNB_QRNN) {
       // carried x for the next call = last input row of this layer (blocked.py:262)
@@ -575,15 +585,42 @@ rnnb_status rnnb_stack_set_highway(rnnb_stack_t h, int layer, int64_t col_offset
   return RNNB_OK;
 }
 
+static rnnb_status forward_impl(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size,
+                                void* H, int64_t ldh, void* c_state, void* x_carry, void* stream);
+
 rnnb_status rnnb_forward(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size, void* H,
                          int64_t ldh, void* c_state, void* x_carry, void* stream) {
   rnnb_status st = check_stack(h);
   if (st != RNNB_OK) return st;
+  if (ldh < (h->layers.empty() ? 1 : h->layers.back().dh)) return fail(RNNB_EINVAL, "ldh smaller than d_h");
+  return forward_impl(h, X, ldx, L, block_size, H, ldh, c_state, x_carry, stream);
+}
+
+rnnb_status rnnb_forward_ex(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size, void* H,
+                            int64_t ldh, void* c_state, void* x_carry, int n_peers, void* const* peer_H,
+                            void* stream) {
+  rnnb_status st = check_stack(h);
+  if (st != RNNB_OK) return st;
+  if ((ldh < 0 ? -ldh : ldh) < h->layers.back().dh) return fail(RNNB_EINVAL, "|ldh| smaller than d_h");
+  if (n_peers < 0 || n_peers > kMaxPeers)
+    return fail(RNNB_EINVAL, "n_peers must be in [0, " + std::to_string(kMaxPeers) + "]");
+  if (n_peers > 0 && !peer_H) return fail(RNNB_EINVAL, "null peer_H");
+  for (int p = 0; p < n_peers; ++p)
+    if (!peer_H[p]) return fail(RNNB_EINVAL, "null peer destination");
+  h->n_peers = n_peers;
+  for (int p = 0; p < n_peers; ++p) h->peer_H[p] = peer_H[p];
+  st = forward_impl(h, X, ldx, L, block_size, H, ldh, c_state, x_carry, stream);
+  h->n_peers = 0;
+  return st;
+}
+
+static rnnb_status forward_impl(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size,
+                                void* H, int64_t ldh, void* c_state, void* x_carry, void* stream) {
+  rnnb_status st = RNNB_OK;
   if (L < 1) return fail(RNNB_EINVAL, "seq_len must be >= 1");
   if (block_size < 1) return fail(RNNB_EINVAL, "block_size must be >= 1");
   if (!X || !H) return fail(RNNB_EINVAL, "null X or H");
   if (ldx < h->layers[0].din) return fail(RNNB_EINVAL, "ldx smaller than d_in");
-  if (ldh < h->layers.back().dh) return fail(RNNB_EINVAL, "ldh smaller than d_h");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int cur = 0;
   cudaGetDevice(&cur);

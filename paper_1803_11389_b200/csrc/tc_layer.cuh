@@ -41,7 +41,9 @@ struct TcArgs {
   const float* Xhw;   // SRU highway source x (fp32, raw), row stride ldhw
   int64_t ldhw;
   float* Hout;        // fp32 h [L][ldh]
-  int64_t ldh;
+  int64_t ldh;        // may be negative (rows stored in reverse time order)
+  float* Hpeer[kMaxPeers];  // same layout as Hout on peer GPUs (mapped), npeer used
+  int npeer;
   void* Hop;          // optional MMA-operand copy of h for the next layer (bf16 or tf32-rounded f32), [L][ldop]
   int64_t ldop;
   const float* bias;  // SRU [Hpad][2] (b_forget, b_highway) or nullptr
@@ -419,7 +421,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             c = rf[j] * c + (1.f - rf[j]) * rz[j];
             float h = ro[j] * tanh_full(c);
             if (CELL == SRU) h = h + (1.f - ro[j]) * a.Xhw[(t0 + j) * a.ldhw + unit];
-            a.Hout[(t0 + j) * a.ldh + unit] = h;
+            store_h(a, (t0 + j) * a.ldh + unit, h);
           }
         }
         if (b == a.nB - 1 && unit < a.Hpad) a.cbuf[unit] = c;  // c_T of the sequence
@@ -470,7 +472,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             c = f[j] * c + (1.f - f[j]) * z[j];
             float h = o[j] * tanh_full(c);
             if (CELL == SRU) h = h + (1.f - o[j]) * a.Xhw[(t0 + col) * a.ldhw + unit];
-            a.Hout[(t0 + col) * a.ldh + unit] = h;
+            store_h(a, (t0 + col) * a.ldh + unit, h);
             if (a.Hop) {
               if (MODE == TC_BF16)
                 reinterpret_cast<__nv_bfloat16*>(a.Hop)[(t0 + col) * a.ldop + unit] = __float2bfloat16_rn(h);

@@ -128,6 +128,19 @@ class DeviceStack:
                                          out.stride(0), cp, xp, _stream_ptr(stream)))
         return out
 
+    def forward_ptr(self, x_ptr, ldx, L, block_size, h_ptr, ldh, peers=(), c_state=None, x_carry=None,
+                    stream=None):
+        """rnnb_forward_ex on raw device addresses (the multi-GPU partitions:
+        X may be a slot of this rank's input ring, H and `peers` mapped peer
+        buffers; ldh < 0 stores rows in reverse time order)."""
+        peers = [int(p) for p in peers]
+        arr = (ctypes.c_void_p * max(1, len(peers)))(*peers) if peers else None
+        cp = ctypes.c_void_p(c_state.data_ptr()) if c_state is not None else None
+        xp = ctypes.c_void_p(x_carry.data_ptr()) if x_carry is not None else None
+        _lib.check(self.lib.rnnb_forward_ex(self._h, ctypes.c_void_p(int(x_ptr)), int(ldx), int(L), int(block_size),
+                                            ctypes.c_void_p(int(h_ptr)), int(ldh), cp, xp, len(peers), arr,
+                                            _stream_ptr(stream)))
+
     def forward_host(self, X, block_size, out=None, c_state=None, x_carry=None, stream=None):
         """End-to-end call on HOST arrays: H2D, forward, D2H inside the C call."""
         X = np.ascontiguousarray(X, dtype=self.np_dtype)
