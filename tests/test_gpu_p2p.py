@@ -137,7 +137,7 @@ def test_p2p_bidir_emulated(mode, tol, world):
     import torch
     import dist_helpers as DH
     from paper_1803_11389_b200 import p2p
-    H, d0, n_layers, L, T_b = 128, 96, 3, 300, 16
+    H, d0, n_layers, L, T_b = 128, 128, 3, 300, 16  # cfg5 shape: d_in == H for layer 1
     fw, bw, _ = DH.make_bidir(H=H, d0=d0, n_layers=n_layers, seed=8)
     X = torch.from_numpy(np.random.default_rng(9).standard_normal((L, d0)).astype(np.float32)).cuda()
     ref = p2p.bidir_reference(fw, bw, X, T_b, mode).cpu().numpy()
