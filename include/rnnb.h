@@ -216,7 +216,9 @@ rnnb_status rnnb_flag_wait(int device, const void* flag, uint32_t value, void* s
  * shared memory, 4 = grid size of `layer`, 5 = dynamic smem bytes,
  * 6 = 1 if the warp-specialised TMA kernel ran `layer`, 7 = pass width NT,
  * 8 = K-chunk staged per pipeline step, 9 = 1 if the tcgen05 tensor-core
- * kernel ran `layer`, 10 = 1 if the register-resident FFMA kernel ran it. */
+ * kernel ran `layer`, 10 = 1 if the register-resident FFMA kernel ran it,
+ * 11 = 1 if the weight-streaming FFMA kernel ran it (weights too large for
+ * shared memory; per-chunk weight images fetched once per 32-step pass). */
 rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value);
 
 #ifdef __cplusplus

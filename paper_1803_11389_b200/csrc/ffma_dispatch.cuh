@@ -34,6 +34,8 @@ struct FfmaPlan {
   bool wsmem = false;
   bool ws = false;  // warp-specialised TMA/mbarrier kernel (ffma_ws.cuh)
   bool reg = false; // register-resident weights kernel (ffma_reg.cuh)
+  bool wstream = false;  // ws kernel with per-chunk weight images streamed through the ring
+  int grid = 0;          // CTAs launched when it differs from ceil(H / U)
   int kc = 0;
   size_t smem = 0;
 };
@@ -194,6 +196,108 @@ static bool try_ws(LayerArgs<TA, TW> a, int grid, cudaStream_t s, FfmaPlan* out,
   return true;
 }
 
+// ---- weight-streaming ws kernel (weights larger than shared memory) ----
+// 32-column passes, kStreamU units per CTA (ceil(2048 / 14) = 147 CTAs for
+// BASELINE cfg4's H = 2048: one CTA per SM), K in chunks of KL*KV columns.
+constexpr int kStreamU = 14;
+
+template <int CELL>
+using WsStreamCfg = WsCfg<float, float, CELL, 32, kStreamU, true>;
+
+template <int CELL>
+inline int ws_stream_kc(int Dp) {
+  const int kc = WsStreamCfg<CELL>::KL * WsStreamCfg<CELL>::KV;
+  return kc < Dp ? kc : Dp;
+}
+
+// [CTA][chunk][tap][kv][Rs][KV] images from the gate-interleaved W [rows][TAPS*Dp]
+template <int CELL>
+__global__ void ws_stream_pack_kernel(const float* __restrict__ W, int rows_src, int Dp, int kc, int nchunk,
+                                      int64_t total, float* __restrict__ out) {
+  using C = WsStreamCfg<CELL>;
+  constexpr int KV = C::KV, Rs = C::Rs, R = C::R, TAPS = C::TAPS;
+  const int nkv = kc / KV;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t q = i;
+    const int e = (int)(q % KV); q /= KV;
+    const int r = (int)(q % Rs); q /= Rs;
+    const int kv = (int)(q % nkv); q /= nkv;
+    const int tap = (int)(q % TAPS); q /= TAPS;
+    const int ch = (int)(q % nchunk); q /= nchunk;
+    const int64_t cta = q;
+    const int64_t row = cta * R + r;
+    const int col = ch * kc + kv * KV + e;
+    out[i] = (r < R && row < rows_src && col < Dp) ? W[row * (int64_t)(TAPS * Dp) + tap * Dp + col] : 0.f;
+  }
+}
+
+template <int CELL>
+size_t ws_stream_elems_t(int Dp, int H) {
+  const int kc = ws_stream_kc<CELL>(Dp);
+  const int nchunk = (Dp + kc - 1) / kc;
+  const int grid = (H + kStreamU - 1) / kStreamU;
+  return (size_t)grid * nchunk * ws_wimg_elems<float, float, CELL, 32, kStreamU, true>(kc);
+}
+
+inline size_t ws_stream_elems(int cell, int Dp, int H) {
+  return cell == SRU ? ws_stream_elems_t<SRU>(Dp, H) : ws_stream_elems_t<QRNN>(Dp, H);
+}
+
+inline cudaError_t ws_stream_pack(int cell, const float* W, int rows_src, int Dp, int H, float* out, cudaStream_t s) {
+  const int64_t total = (int64_t)ws_stream_elems(cell, Dp, H);
+  const int bs = 256;
+  const int grid = (int)((total + bs - 1) / bs < 148 * 32 ? (total + bs - 1) / bs : 148 * 32);
+  if (cell == SRU) {
+    const int kc = ws_stream_kc<SRU>(Dp);
+    ws_stream_pack_kernel<SRU><<<grid, bs, 0, s>>>(W, rows_src, Dp, kc, (Dp + kc - 1) / kc, total, out);
+  } else {
+    const int kc = ws_stream_kc<QRNN>(Dp);
+    ws_stream_pack_kernel<QRNN><<<grid, bs, 0, s>>>(W, rows_src, Dp, kc, (Dp + kc - 1) / kc, total, out);
+  }
+  return cudaGetLastError();
+}
+
+template <typename TA, typename TW, int CELL>
+static bool try_ws_stream(LayerArgs<TA, TW> a, cudaStream_t s, FfmaPlan* out, cudaError_t* err) {
+  if constexpr (!(sizeof(TA) == 4 && sizeof(TW) == 4)) {
+    return false;
+  } else {
+    if (!ws_eligible(a) || a.Wst == nullptr) return false;
+    constexpr int NT = 32, U = kStreamU;
+    using WC = WsStreamCfg<CELL>;
+    constexpr int BWMAX = 512 / (int)sizeof(TA);
+    const int kc = ws_stream_kc<CELL>(a.Dp);
+    int bw = WC::KV;
+    while (bw < kc && bw < BWMAX) bw <<= 1;
+    const int nbox = (kc + bw - 1) / bw;
+    const size_t sm = ws_smem_bytes<TA, TW, CELL, NT, U, true>(a.Dp, nbox * bw, bw);
+    if (sm > kMaxSmem) return false;
+    CUtensorMap tm;
+    if (!make_x_map<TA>(&tm, a.X, a.D, a.L, a.ldx, bw + WC::PADV, NT + 1)) return false;
+    a.KC = kc;
+    a.KCB = bw;
+    auto k = ffma_ws_kernel<TA, TW, CELL, NT, U, XR_NONE, false, true>;
+    static bool attr_done = false;
+    if (!attr_done) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem);
+      if (e != cudaSuccess) {
+        *err = e;
+        return true;
+      }
+      attr_done = true;
+    }
+    const int grid = (a.H + U - 1) / U;
+    k<<<grid, WC::THREADS, sm, s>>>(a, tm);
+    *err = cudaGetLastError();
+    if (out) {
+      FfmaPlan p;
+      p.nt = NT; p.wsmem = false; p.ws = true; p.wstream = true; p.kc = kc; p.smem = sm; p.grid = grid;
+      *out = p;
+    }
+    return true;
+  }
+}
+
 template <typename TA, typename TW, int CELL, int NT, int U>
 static cudaError_t run_nt(LayerArgs<TA, TW> a, int grid, bool allow_wsmem, cudaStream_t s, FfmaPlan* out) {
   if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4 && (U == 7 || U == 4)) {
@@ -232,6 +336,10 @@ static cudaError_t run_u(const LayerArgs<TA, TW>& a, int grid, bool allow_wsmem,
       // Falls back to NT = 16 when its shared-memory plan does not fit
       // (RNNB_NT32=0 forces NT = 16).
       if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4) {
+        if (a.Wst != nullptr && a.T_b >= 32 && a.xround == XR_NONE && a.x_ready == nullptr) {
+          cudaError_t e;
+          if (try_ws_stream<TA, TW, CELL>(a, s, out, &e)) return e;
+        }
         const char* env = getenv("RNNB_NT32");
         if (allow_wsmem && a.T_b >= 32 && a.xround == XR_NONE && !(env && env[0] == '0')) {
           cudaError_t e;

@@ -60,6 +60,9 @@ struct LayerArgs {
   int* h_done;
   int h_chunk;
   int* stream_fail;    // set by the kernel if streamed rows did not arrive in time
+  // weight-streaming ws kernel (layers whose weights do not fit in shared
+  // memory): per-(CTA, chunk) weight images, see ws_stream_pack
+  const TW* Wst;
 };
 
 constexpr int kThreads = 256;

@@ -48,6 +48,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t tx
                "r"(tx)
                : "memory");
 }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t tx) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(tx) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -150,13 +153,16 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // tile (CT = 4, fp32, NT >= 16) halves the LDS per FMA of the narrow one;
 // it needs ~2x the accumulator registers, so it runs 8 consumer warps
 // (KG = 4) with up to 168 registers each instead of 16 with 96.
-template <typename TA, typename TW, int CELL, int NT, int U>
+template <typename TA, typename TW, int CELL, int NT, int U, bool WSTR = false>
 struct WsCfg {
   static constexpr int KV = 16 / (int)sizeof(TA);
   static constexpr int TAPS = CELL == QRNN ? 2 : 1;
   static constexpr int R = 3 * U;
   static constexpr int CTW = (sizeof(TA) == 4 && NT >= RNNB_WIDE_MIN_NT) ? 4 : 2;
-  static constexpr int KG = CTW == 4 ? 4 : 8, RG = 2;
+  // more rows per CTA (U = 14, weight-streaming layers) -> more row groups,
+  // same per-warp tile and warp count
+  static constexpr int RG = R > 24 ? 4 : 2;
+  static constexpr int KG = (CTW == 4 ? 8 : 16) / RG;
   static constexpr int CW = KG * RG;                       // consumer warps
   static constexpr int THREADS = (CW + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group
   static constexpr int RH = (R + RG - 1) / RG;
@@ -177,7 +183,9 @@ struct WsCfg {
   // (also the short fp32 passes, NT <= 8, where a pass lasts ~1 us and the
   // buffers cost < 3 KB)
   static constexpr int NRED = (NT == 32 || (sizeof(TA) == 4 && NT <= 8)) ? 2 : 1;
-  static constexpr int STAGES = NT == 32 ? 3 : 4;
+  // WSTR: weights are not resident, so the ring can be deeper; each stage
+  // also carries the chunk's weight image
+  static constexpr int STAGES = WSTR ? 6 : (NT == 32 ? 3 : 4);
   // reduce-scatter over the LANES_K lanes of a k-group: NV partials per lane
   // (padded to a multiple of LANES_K), NV / LANES_K sums per lane afterwards
   static constexpr int NV = (RH * CT + LANES_K - 1) / LANES_K * LANES_K;
@@ -185,17 +193,27 @@ struct WsCfg {
 
 // x chunk of KC columns = KC/BW TMA boxes of [NT+1 rows x (BW + PADV) cols],
 // each box at a 128-byte aligned stride inside the stage buffer
-template <typename TA, typename TW, int CELL, int NT, int U>
+template <typename TA, typename TW, int CELL, int NT, int U, bool WSTR = false>
 __host__ __device__ inline size_t ws_box_elems(int BW) {
-  using C = WsCfg<TA, TW, CELL, NT, U>;
+  using C = WsCfg<TA, TW, CELL, NT, U, WSTR>;
   return align_up((size_t)(NT + 1) * (BW + C::PADV), 128 / sizeof(TA));
 }
 
-template <typename TA, typename TW, int CELL, int NT, int U>
+// WSTR: one chunk's weight image in global memory and in a stage, elements:
+// [tap][kv of the chunk][Rs][KV] (the resident layout restricted to a chunk)
+template <typename TA, typename TW, int CELL, int NT, int U, bool WSTR = false>
+__host__ __device__ inline size_t ws_wimg_elems(int KC) {
+  using C = WsCfg<TA, TW, CELL, NT, U, WSTR>;
+  return (size_t)C::TAPS * (KC / C::KV) * C::Rs * C::KV;
+}
+
+template <typename TA, typename TW, int CELL, int NT, int U, bool WSTR = false>
 __host__ __device__ inline size_t ws_smem_bytes(int Dp, int KC, int BW) {
-  using C = WsCfg<TA, TW, CELL, NT, U>;
-  size_t off = align_up((size_t)C::TAPS * Dp / C::KV * C::Rs * C::KV * sizeof(TW) + 16 * C::RG, 128);
-  off += (size_t)C::STAGES * (KC / BW) * ws_box_elems<TA, TW, CELL, NT, U>(BW) * sizeof(TA);
+  using C = WsCfg<TA, TW, CELL, NT, U, WSTR>;
+  size_t off = WSTR ? 0 : align_up((size_t)C::TAPS * Dp / C::KV * C::Rs * C::KV * sizeof(TW) + 16 * C::RG, 128);
+  off += (size_t)C::STAGES * align_up(((KC + BW - 1) / BW) * ws_box_elems<TA, TW, CELL, NT, U, WSTR>(BW) * sizeof(TA) +
+                                          (WSTR ? ws_wimg_elems<TA, TW, CELL, NT, U, WSTR>(KC) * sizeof(TW) : 0),
+                                      128);
   off += (size_t)C::NRED * C::KG * C::Rpad * NT * sizeof(TA);
   off += (size_t)3 * U * NT * sizeof(TA);
   off = align_up(off, 8);
@@ -205,10 +223,14 @@ __host__ __device__ inline size_t ws_smem_bytes(int Dp, int KC, int BW) {
 
 // STREAM: X arrives while the kernel runs (rnnb_forward_host streaming); a
 // separate instantiation so the plain kernel's code is untouched.
-template <typename TA, typename TW, int CELL, int NT, int U, int XR, bool STREAM = false>
-__global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
+// WSTR: the layer's weights do not fit in shared memory (BASELINE cfg4 fp32):
+// each stage of the ring also carries the chunk's weight image, bulk-copied
+// from a pre-tiled copy (a.Wst: [CTA][chunk][tap][kv][Rs][KV]), so every
+// weight is fetched once per pass of NT columns.
+template <typename TA, typename TW, int CELL, int NT, int U, int XR, bool STREAM = false, bool WSTR = false>
+__global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
     ffma_ws_kernel(LayerArgs<TA, TW> a, const __grid_constant__ CUtensorMap tmx) {
-  using C = WsCfg<TA, TW, CELL, NT, U>;
+  using C = WsCfg<TA, TW, CELL, NT, U, WSTR>;
   constexpr int KV = C::KV, TAPS = C::TAPS, R = C::R, Rs = C::Rs, KG = C::KG, RH = C::RH, Rpad = C::Rpad;
   constexpr int LANES_T = C::LANES_T, CT = C::CT, LANES_K = C::LANES_K, KL = C::KL;
   constexpr int STAGES = C::STAGES;
@@ -218,16 +240,19 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
   const int BXS = BW + C::PADV;          // padded row pitch inside a box
   const int LVPB = __ffs(BW / KV) - 1;   // log2(k-vectors per box); BW is a power of 2
   const int MVPB = BW / KV - 1;
-  const int BOXS = (int)ws_box_elems<TA, TW, CELL, NT, U>(BW);
+  const int BOXS = (int)ws_box_elems<TA, TW, CELL, NT, U, WSTR>(BW);
   const int Dp = a.Dp;
   const int Kv = TAPS * Dp / KV;  // k-vectors per row
 
   extern __shared__ __align__(128) unsigned char smem[];
   size_t off = 0;
   TW* Ws = reinterpret_cast<TW*>(smem);
-  off = align_up((size_t)Kv * Rs * KV * sizeof(TW) + 16 * C::RG, 128);  // TMA dst: 128-B aligned
+  if constexpr (!WSTR) off = align_up((size_t)Kv * Rs * KV * sizeof(TW) + 16 * C::RG, 128);  // TMA dst: 128-B aligned
   TA* Xr = reinterpret_cast<TA*>(smem + off);
-  const size_t stage_bytes = (size_t)((KC + BW - 1) / BW) * BOXS * sizeof(TA);
+  const size_t xstage_bytes = (size_t)((KC + BW - 1) / BW) * BOXS * sizeof(TA);
+  const size_t wimg_elems = WSTR ? ws_wimg_elems<TA, TW, CELL, NT, U, WSTR>(KC) : 0;
+  // stage = x boxes [+ weight image]; the weight image follows the boxes
+  const size_t stage_bytes = align_up(xstage_bytes + wimg_elems * sizeof(TW), 128);
   off += (size_t)STAGES * stage_bytes;
   constexpr int NRED = C::NRED;
   constexpr size_t red_elems = (size_t)KG * Rpad * NT;
@@ -247,7 +272,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
   const TW* Wg = a.W + (size_t)u0 * 3 * TAPS * Dp;
 
   // weights -> Ws[kv][r][:], once per launch (rows of Wg are [R][Kp])
-  {
+  if constexpr (!WSTR) {
     constexpr int VB = KV * (int)sizeof(TW);  // bytes per (kv, r) vector
     const int nvec = R * Kv;
     for (int i = tid; i < nvec; i += NTHR) {
@@ -301,6 +326,15 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
           TA* xb = reinterpret_cast<TA*>(reinterpret_cast<char*>(Xr) + (size_t)s * stage_bytes);
           const bool carry_row = (r0 == 0 && tp == 0 && a.xcarry != nullptr);
+          if constexpr (WSTR) {
+            // this chunk's weight image: one bulk copy, counted on the same barrier
+            if (lane == 0) {
+              const uint32_t wb = (uint32_t)(wimg_elems * sizeof(TW));
+              mbar_expect_tx(&full[s], wb);  // no arrival: the x copies below arrive once
+              const TW* src = a.Wst + ((size_t)blockIdx.x * nchunk + (size_t)(d0 / KC)) * wimg_elems;
+              bulk_g2s(reinterpret_cast<char*>(xb) + xstage_bytes, src, wb, &full[s]);
+            }
+          }
           if (!carry_row) {
             // one 2-D TMA box [NT+1-r0 rows x XS cols] per chunk: box rows land at
             // pitch XS (the padding columns are real neighbours, never read), rows
@@ -349,7 +383,8 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           for (int w = 0; w < KG; ++w) s += redb[((size_t)w * Rpad + r) * NT + col];
           const int u = r / 3, g = r - 3 * (r / 3);
           TA v;
-          if (CELL == SRU) v = g == 0 ? s : sigmoid_ref<TA>(s + a.bias[(size_t)(u0 + u) * 2 + g - 1]);
+          if (CELL == SRU)
+            v = g == 0 ? s : sigmoid_ref<TA>(s + (u0 + u < a.H ? a.bias[(size_t)(u0 + u) * 2 + g - 1] : TA(0)));
           else v = g == 0 ? tanh_full(s) : sigmoid_ref<TA>(s);
           gate[((size_t)g * U + u) * NT + col] = v;
         }
@@ -396,8 +431,14 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
     const int xlane = (kl >> LVPB) * BOXS + (tq + 1) * BXS + (kl & MVPB) * KV;
     const TA* xlane_base = Xr + xlane;
     const size_t stage_elems = stage_bytes / sizeof(TA);
-    const TW* wlane_base = Ws + ((size_t)kl * Rs + rbase) * KV;
+    const TW* wlane_base = WSTR ? reinterpret_cast<const TW*>(reinterpret_cast<const char*>(Xr) + xstage_bytes) +
+                                      ((size_t)kl * Rs + rbase) * KV
+                                : Ws + ((size_t)kl * Rs + rbase) * KV;
     const size_t w_chunk = (size_t)(KC / KV) * Rs * KV;  // weights of one chunk (all rows)
+    // tap stride inside the weights a lane reads: the resident array holds all
+    // of K per tap, a streamed chunk image one chunk per tap
+    const size_t w_tap = WSTR ? w_chunk : (size_t)(Dp / KV) * Rs * KV;
+    const size_t stage_tw = stage_bytes / sizeof(TW);
     const int kv_last = (Dp - (nchunk - 1) * KC) / KV;    // k-vectors in the last chunk
     uint32_t seq = 0, pass = 0;
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
@@ -434,10 +475,10 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U>::THREADS, 1)
           // last chunk of a row can be partial
           if (ccur != nchunk - 1 || kl < kv_last) {
             const TA* xl = xlane_base + (size_t)s * stage_elems;
-            const TW* wl = wlane_base + (size_t)ccur * w_chunk;
+            const TW* wl = WSTR ? wlane_base + (size_t)s * stage_tw : wlane_base + (size_t)ccur * w_chunk;
 #pragma unroll
             for (int tap = 0; tap < TAPS; ++tap) {
-              const TW* wp = wl + (size_t)tap * (Dp / KV) * Rs * KV;
+              const TW* wp = wl + (size_t)tap * w_tap;
               if constexpr (kPacked) {
                 ulonglong2 xp[CT];
 #pragma unroll

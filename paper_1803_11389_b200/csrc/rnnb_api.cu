@@ -61,6 +61,9 @@ struct Layer {
   bool last_tc = false;
   float* bias_tc = nullptr;  // [Hpad128][2]
   int64_t hw_off = 0;        // SRU highway reads x[:, hw_off + unit] (wide / sharded SRU)
+  // fp32 layers too large for shared memory: per-(CTA, chunk) weight images
+  // for the weight-streaming ws kernel, built on first use (ws_stream_pack)
+  void* Wst = nullptr;
 };
 
 }  // namespace
@@ -289,6 +292,23 @@ rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_
   Layer& ly = h->layers[li];
   ly.last_tc = false;
   LayerArgs<TA, TW> a = make_args<TA, TW>(h, ly);
+  if constexpr (sizeof(TA) == 4 && sizeof(TW) == 4) {
+    // weights beyond what a CTA can keep in shared memory: stream per-chunk
+    // weight images through the ws kernel's ring (T_b >= 32 passes)
+    const size_t res_bytes = (size_t)3 * ly.U * taps(h->kind) * ly.Dp * sizeof(float);
+    const char* env = getenv("RNNB_WSTREAM");
+    if (G == nullptr && Tb >= 32 && a.xround == XR_NONE && h->stream_ready == nullptr &&
+        res_bytes + 44 * 1024 > kMaxSmem && !(env && env[0] == '0') && ly.din % 8 == 0) {
+      // (the resident plans need ~44 KB of ring + partials beside the weights)
+      if (!ly.Wst) {
+        const size_t n = ws_stream_elems(h->kind, ly.Dp, (int)ly.dh);
+        CUDA_TRY(cudaMalloc(&ly.Wst, n * sizeof(float)));
+        CUDA_TRY(ws_stream_pack(h->kind, static_cast<const float*>(ly.W), 3 * ly.Upad, ly.Dp, (int)ly.dh,
+                                static_cast<float*>(ly.Wst), s));
+      }
+      a.Wst = static_cast<const TW*>(ly.Wst);
+    }
+  }
   a.X = X;
   a.ldx = ldx;
   a.xcarry = h->kind == RNNB_QRNN ? xc_io : nullptr;
@@ -310,7 +330,7 @@ rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_
   }
   if (e != cudaSuccess) return cuda_fail(e, "ffma_layer launch");
   ly.last = plan;
-  ly.grid = (int)((ly.dh + ly.U - 1) / ly.U);
+  ly.grid = plan.grid ? plan.grid : (int)((ly.dh + ly.U - 1) / ly.U);
   h->last_launches += 1;
   return RNNB_OK;
 }
@@ -451,6 +471,7 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   cudaSetDevice(h->device);
   for (auto& ly : h->layers) {
     if (ly.W) cudaFree(ly.W);
+    if (ly.Wst) cudaFree(ly.Wst);
     if (ly.bias) cudaFree(ly.bias);
     if (ly.Wtc) cudaFree(ly.Wtc);
     if (ly.bias_tc) cudaFree(ly.bias_tc);
@@ -512,6 +533,7 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
   cudaGetDevice(&cur);
   CUDA_TRY(cudaSetDevice(h->device));
   if (ly.W) cudaFree(ly.W), ly.W = nullptr;
+  if (ly.Wst) cudaFree(ly.Wst), ly.Wst = nullptr;  // rebuilt from the new weights on first use
   if (ly.bias) cudaFree(ly.bias), ly.bias = nullptr;
   ly.wbytes = host.size();
   CUDA_TRY(cudaMalloc(&ly.W, host.size()));
@@ -896,6 +918,7 @@ rnnb_status rnnb_query(rnnb_stack_t h, int what, int layer, int64_t* value) {
     case 8: *value = h->layers[layer].last.kc; return RNNB_OK;
     case 9: *value = h->layers[layer].last_tc ? 1 : 0; return RNNB_OK;
     case 10: *value = h->layers[layer].last.reg ? 1 : 0; return RNNB_OK;
+    case 11: *value = h->layers[layer].last.wstream ? 1 : 0; return RNNB_OK;
     default: return fail(RNNB_EINVAL, "unknown query");
   }
 }

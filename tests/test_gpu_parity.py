@@ -504,3 +504,35 @@ def test_host_streaming_matches_device(P, oracle, kind, d, L, T, monkeypatch):
         H3 = st.forward_host(X, T)
         assert H2.tobytes() == H3.tobytes()
     st.close()
+
+
+@pytest.mark.parametrize("kind,d,n_layers", [("qrnn", 2048, 2), ("sru", 4096, 1), ("qrnn", 1536, 1), ("sru", 2056, 1)])
+def test_weight_streaming_kernel(P, oracle, kind, d, n_layers, monkeypatch):
+    """fp32 layers whose weights do not fit in shared memory (BASELINE cfg4:
+    QRNN 2048, 100 MB per layer): the ws kernel with per-(CTA, chunk) weight
+    images streamed through its ring (14 units per CTA), T_b >= 32, incl. a
+    remainder block, carried state and an H not a multiple of 14, vs the
+    oracle and vs the generic kernel (RNNB_WSTREAM=0)."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, n_layers, 81, np.float32)
+    L = 203
+    X = np.random.default_rng(19).standard_normal((L, d)).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    st = P.DeviceStack(kind, layers)
+    for T in (32, 48, 64):
+        H = st.forward(Xd, T).cpu().numpy()
+        assert all(st.query(11, li) == 1 for li in range(n_layers)), T
+        ref = oracle.run_blocked(kind, layers, X, T)
+        assert_f32(H, ref)
+    # chunked with carried state == one call (same kernel, same per-unit order)
+    c = torch.zeros(d * n_layers, device="cuda")
+    xc = torch.zeros(d * n_layers, device="cuda")
+    a = st.forward(Xd[:96], 32, c_state=c, x_carry=xc if kind == "qrnn" else None)
+    b = st.forward(Xd[96:], 32, c_state=c, x_carry=xc if kind == "qrnn" else None)
+    whole = st.forward(Xd, 32).cpu().numpy()
+    assert np.concatenate([a.cpu().numpy(), b.cpu().numpy()]).tobytes() == whole.tobytes()
+    monkeypatch.setenv("RNNB_WSTREAM", "0")
+    G = st.forward(Xd, 32).cpu().numpy()
+    assert st.query(11) == 0
+    assert_f32(G, whole)
+    st.close()
