@@ -154,6 +154,14 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
             src += "; algorithmic FLOPs only (3 tf32 products per fp32 product executed)"
     achieved = flops / sec / 1e12
     hbm = pk["hbm_gbs"]
+    # weight-stream roofline: the tensor-core kernel fetches every weight tile
+    # from L2 once per block (the same bytes as the cold-cache model); rated
+    # against the L2 read throughput measured by tools/l2_peak.cu
+    l2 = None
+    lp = os.path.join(REPO, "profiles", "l2_peak.json")
+    if os.path.exists(lp):
+        with open(lp) as f:
+            l2 = json.load(f)["l2_read_gbs"]
     return {
         "bound": "tensor" if tc else "compute",
         "pipe": pipe,
@@ -166,6 +174,11 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
                     "the kernel keeps the weight slice SMEM/L2-resident, so this exceeds real DRAM traffic",
             "bytes_per_launch": bytes_model, "achieved_gbs": round(bytes_model / sec / 1e9, 1),
             "peak_gbs": hbm, "frac": round(bytes_model / sec / 1e9 / hbm, 4)},
+        "l2_model": None if l2 is None else {
+            "note": "same bytes against the measured L2 read throughput (profiles/l2_peak.json): the bound of "
+                    "the tensor-core kernel, which streams each weight tile from L2 once per block",
+            "achieved_gbs": round(bytes_model / sec / 1e9, 1), "peak_gbs": l2,
+            "frac": round(bytes_model / sec / 1e9 / l2, 4)},
     }
 
 
@@ -306,7 +319,8 @@ def run_ours(args, rank, world, local_rank):
             out_[str(T_b)] = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
                               "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"],
                               "tflops": rf["achieved"], "pipe": rf["pipe"], "kernel": kernel_name(r),
-                              "hbm_model_frac": rf["hbm_model"]["frac"]}
+                              "hbm_model_frac": rf["hbm_model"]["frac"],
+                              "l2_model_frac": rf["l2_model"]["frac"] if rf["l2_model"] else None}
         return out_
 
     head = results[args.block]
