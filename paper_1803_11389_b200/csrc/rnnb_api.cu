@@ -76,7 +76,10 @@ struct rnnb_stack {
   int64_t last_launches = 0;
   void* op = nullptr;     // tensor-core operand copy of a layer input, [L+1][maxD]
   size_t op_bytes = 0;
-  float* cbuf = nullptr;  // tensor-core c chain state + flags
+  float* cbuf = nullptr;  // tensor-core c_T scratch + look-back state + status words
+  int tc_epoch = 0;       // launch tag of the look-back status words
+  int* tc_status = nullptr;  // [capacity] status words, cleared only on (re)allocation
+  size_t tc_status_n = 0;
   int* flags = nullptr;
   size_t cf_bytes = 0;
   void* hostX = nullptr;  // e2e device staging
@@ -226,9 +229,9 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   }
   const int nU = ly.Hpad128 / 128;
   const int64_t nB = (L + Tb - 1) / Tb;
-  // cbuf [Hpad] | aggA, aggB, incl [nB][Hpad] | status [nB][nU]
+  // cbuf [Hpad] (c_T scratch) | aggA, aggB, incl [nB][Hpad]: written before read
   const size_t plane = (size_t)nB * ly.Hpad128;
-  const size_t cfb = ((size_t)ly.Hpad128 + 3 * plane) * sizeof(float) + (size_t)nB * nU * sizeof(int);
+  const size_t cfb = ((size_t)ly.Hpad128 + 3 * plane) * sizeof(float);
   if (h->cf_bytes < cfb) {
     if (h->cbuf) cudaFree(h->cbuf);
     h->cbuf = nullptr;
@@ -237,11 +240,24 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
     h->cf_bytes = cfb;
   }
   float* aggA = h->cbuf + ly.Hpad128;
-  int* status = reinterpret_cast<int*>(aggA + 3 * plane);
+  // status words [nB][nU] in their own allocation, cleared only when it is
+  // (re)allocated: each launch tags its statuses 4*epoch + state, so anything
+  // an earlier launch left (any layer, any layout) reads as "not yet"
+  const size_t nst = (size_t)nB * nU;
+  if (h->tc_status_n < nst || h->tc_epoch >= (1 << 28)) {
+    if (h->tc_status_n < nst) {
+      if (h->tc_status) cudaFree(h->tc_status);
+      h->tc_status = nullptr;
+      h->tc_status_n = 0;
+      CUDA_TRY(cudaMalloc(&h->tc_status, nst * sizeof(int)));
+      h->tc_status_n = nst;
+    }
+    CUDA_TRY(cudaMemsetAsync(h->tc_status, 0, h->tc_status_n * sizeof(int), s));
+    h->tc_epoch = 0;
+  }
+  int* status = h->tc_status;
+  ++h->tc_epoch;
   CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s));
-  CUDA_TRY(cudaMemsetAsync(h->cbuf, 0, ly.Hpad128 * sizeof(float), s));
-  CUDA_TRY(cudaMemsetAsync(status, 0, (size_t)nB * nU * sizeof(int), s));
-  if (c_io) CUDA_TRY(cudaMemcpyAsync(h->cbuf, c_io, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
   TcArgs a{};
   a.Xhw = X + ly.hw_off;
   a.ldhw = ldx;
@@ -251,7 +267,9 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.npeer = h->cur_peers;
   for (int p = 0; p < h->cur_peers; ++p) a.Hpeer[p] = static_cast<float*>(h->peer_H[p]);
   a.bias = ly.bias_tc;
-  a.cbuf = h->cbuf;
+  a.c_in = c_io;                          // read only (anchor of the look-back)
+  a.c_out = c_io ? h->cbuf : nullptr;     // c_T to scratch, copied to c_io after the launch
+  a.epoch = h->tc_epoch;
   a.aggA = aggA;
   a.aggB = aggA + plane;
   a.incl = aggA + 2 * plane;
@@ -478,6 +496,7 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   }
   if (h->op) cudaFree(h->op);
   if (h->cbuf) cudaFree(h->cbuf);
+  if (h->tc_status) cudaFree(h->tc_status);
   for (auto& p : h->ws)
     if (p) cudaFree(p);
   if (h->hostX) cudaFree(h->hostX);

@@ -47,8 +47,11 @@ struct TcArgs {
   void* Hop;          // optional MMA-operand copy of h for the next layer (bf16 or tf32-rounded f32), [L][ldop]
   int64_t ldop;
   const float* bias;  // SRU [Hpad][2] (b_forget, b_highway) or nullptr
-  float* cbuf;        // [Hpad] carried c state (in: c_0, out: c_T)
-  int* status;        // [nB][nU] look-back status: 0 none, 1 aggregate, 2 inclusive
+  const float* c_in;  // [H] c_0 (nullptr: zeros); never written by the launch
+  float* c_out;       // [H] c_T (nullptr: not written); must not alias c_in
+  int* status;        // [nB][nU] look-back status: 4*epoch + {1 aggregate, 2 inclusive}
+  int epoch;          // this launch's tag: values of earlier launches read as "none"
+                      // (no per-launch clearing of the status array)
   float* aggA;        // [nB][Hpad] block carry map c_out = A c_in + B
   float* aggB;
   float* incl;        // [nB][Hpad] c after the block (inclusive prefix)
@@ -184,14 +187,15 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
   a.aggB[sidx] = Bblk;
   __threadfence();
   tc_epi_sync();
-  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 1);
+  const int tag = 4 * a.epoch;
+  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 1);
   const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
   // lanes of the first epilogue warp wait for the statuses in parallel
   if (et < 32) {
     const int j = b - 1 - et;
-    if (j >= jlo) while (ld_acquire(&a.status[(size_t)j * a.nU + u]) < 1) __nanosleep(32);
+    if (j >= jlo) while (ld_acquire(&a.status[(size_t)j * a.nU + u]) < tag + 1) __nanosleep(32);
     const int jb = jlo - 1;  // block whose inclusive carry anchors the chain
-    if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < 2) __nanosleep(32);
+    if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < tag + 2) __nanosleep(32);
   }
   tc_epi_sync();
   float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
@@ -201,12 +205,13 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
     Bacc = Aacc * Bj + Bacc;
     Aacc = Aacc * Aj;
   }
-  const float anchor = jlo > 0 ? ld_cg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit]) : ld_cg(&a.cbuf[unit]);
+  const float anchor = jlo > 0 ? ld_cg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit])
+                                : (a.c_in != nullptr && unit < a.H ? a.c_in[unit] : 0.f);
   const float cin = Aacc * anchor + Bacc;
   a.incl[sidx] = Ablk * cin + Bblk;
   __threadfence();
   tc_epi_sync();
-  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], 2);
+  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
   return cin;
 }
 
@@ -424,7 +429,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             store_h(a, (t0 + j) * a.ldh + unit, h);
           }
         }
-        if (b == a.nB - 1 && unit < a.Hpad) a.cbuf[unit] = c;  // c_T of the sequence
+        if (b == a.nB - 1 && a.c_out != nullptr && unit < a.H) a.c_out[unit] = c;  // c_T of the sequence
         continue;
       }
       const int ab = acc_it % C::NACC;
@@ -486,7 +491,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_before();
       mbar_arrive(&acc_empty[ab]);
       ++acc_it;
-      if (b == a.nB - 1 && unit < a.Hpad) a.cbuf[unit] = c;  // c_T of the sequence
+      if (b == a.nB - 1 && a.c_out != nullptr && unit < a.H) a.c_out[unit] = c;  // c_T of the sequence
     }
   }
   tc_fence_before();
