@@ -725,10 +725,14 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
   char* hH = static_cast<char*>(H);
   char* dH = static_cast<char*>(h->hostH);
   const int64_t T = block_size < 1 ? 1 : block_size;
-  if (c_state) CUDA_TRY(cudaMemcpyAsync(dC, c_state, csz * es, cudaMemcpyHostToDevice, s));
-  else CUDA_TRY(cudaMemsetAsync(dC, 0, csz * es, s));
-  if (x_carry) CUDA_TRY(cudaMemcpyAsync(dXC, x_carry, xsz * es, cudaMemcpyHostToDevice, s));
-  else CUDA_TRY(cudaMemsetAsync(dXC, 0, xsz * es, s));
+  if (!c_state && !x_carry) {
+    CUDA_TRY(cudaMemsetAsync(dC, 0, (csz + xsz) * es, s));  // dC, dXC are adjacent: one call
+  } else {
+    if (c_state) CUDA_TRY(cudaMemcpyAsync(dC, c_state, csz * es, cudaMemcpyHostToDevice, s));
+    else CUDA_TRY(cudaMemsetAsync(dC, 0, csz * es, s));
+    if (x_carry) CUDA_TRY(cudaMemcpyAsync(dXC, x_carry, xsz * es, cudaMemcpyHostToDevice, s));
+    else CUDA_TRY(cudaMemsetAsync(dXC, 0, xsz * es, s));
+  }
   cudaEvent_t ev_start = h->ev[16], ev_done = h->ev[17];
 
   // Streaming (single-layer fp32 stacks, warp-specialised kernel): ONE layer
@@ -765,17 +769,24 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
       h->stream_done = h->stream_ctr + 2;
       h->stream_chunk = (int)sc;
       h->stream_refused = false;
+      // chunk 0's copy-in first: its rows land while the layer kernel is
+      // still being launched and loads its weights (the kernel polls the
+      // counter); if the layer cannot stream, the chunked path below copies again
+      auto copy_in = [&](int64_t i) -> rnnb_status {
+        const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
+        CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice,
+                                 h->s_in));
+        CU_TRY(so.write(h->s_in, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
+        return RNNB_OK;
+      };
+      if ((st = copy_in(0)) != RNNB_OK) return st;
       st = rnnb_forward(h, dX, din, L, block_size, dH, dh, dC, dXC, stream);
       h->stream_ready = nullptr;
       h->stream_done = nullptr;
       if (st == RNNB_OK) {
         const unsigned grid = (unsigned)h->layers[0].grid;
-        for (int64_t i = 0; i < nsc; ++i) {
-          const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
-          CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice,
-                                   h->s_in));
-          CU_TRY(so.write(h->s_in, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
-        }
+        for (int64_t i = 1; i < nsc; ++i)
+          if ((st = copy_in(i)) != RNNB_OK) return st;
         for (int64_t i = 0; i < nsc; ++i) {
           const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
           CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 2 + i), grid, CU_STREAM_WAIT_VALUE_GEQ));

@@ -37,3 +37,15 @@ ts = np.array(ts) * 1e3
 L = w.seq_len
 print(f"{a.tag} {a.workload} {a.mode} T_b={a.block}: mean {ts.mean():.4f} ms ({L / ts.mean() * 1e-3:.3f} M steps/s) "
       f"median {np.median(ts):.4f} min {ts.min():.4f} max {ts.max():.4f}", flush=True)
+
+if os.environ.get("E2E_TIMELINE"):
+    # CUPTI timeline of one call: start/end of every copy and kernel relative to the first activity
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA, torch.profiler.ProfilerActivity.CPU]) as prof:
+        t0 = time.perf_counter()
+        st.forward_host(Xn, a.block, out=Hn)
+        t1 = time.perf_counter()
+    evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    base = min(e.time_range.start for e in evs)
+    print(f"wall {(t1 - t0) * 1e6:.1f} us; device span {max(e.time_range.end for e in evs) - base:.1f} us")
+    for e in sorted(evs, key=lambda e: e.time_range.start):
+        print(f"  {e.time_range.start - base:9.1f} .. {e.time_range.end - base:9.1f}  {e.name[:60]}")
