@@ -133,6 +133,20 @@ rnnb_status rnnb_sweep(const void* forget, const void* cand, const void* c_init,
 rnnb_status rnnb_finalize(int kind, const void* out_gate, const void* C, const void* Xb, void* H,
                           int64_t d, int64_t T, int dtype, void* stream);
 
+/* Unit-level dense kernels of kernels.py on DEVICE buffers (row-major,
+ * leading dimensions in elements):
+ *   rnnb_gemm  gemm / gemv (kernels.py:181-233): C[m x n] = A[m x k] B[k x n]
+ *              (gemv: n = 1).  strict != 0 ("reference", "tiled"): ascending
+ *              inner index, separately rounded multiply and add -- bitwise the
+ *              reference kernels' chain (kernels.py:55-113); strict == 0
+ *              ("fast"): fused multiply-add, tolerance-checked like
+ *              kernels.py:116-178.
+ *   rnnb_activation  sigmoid (which = 0; 0.5 (1 + tanh(x/2)), kernels.py:236)
+ *              or tanh (which = 1, kernels.py:240), elementwise, y may == x. */
+rnnb_status rnnb_gemm(int strict, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
+                      int64_t ldc, int64_t m, int64_t n, int64_t k, int dtype, void* stream);
+rnnb_status rnnb_activation(int which, const void* x, void* y, int64_t n, int dtype, void* stream);
+
 /* ---- LSTM partial precompute ----
  * lstm_run_precomputed(w, X, block_size)  blocked.py:271-305, one layer:
  * input-side products W x + b for the sequence (one GEMM launch), then the

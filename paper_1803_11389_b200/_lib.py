@@ -26,6 +26,7 @@ SYMBOLS = (
     "rnnb_stack_load_rnnw", "rnnb_lstm_load_rnnw", "rnnb_rnnx_info", "rnnb_rnnx_load",
     "rnnb_forward_ex", "rnnb_dev_alloc", "rnnb_dev_free", "rnnb_ipc_handle", "rnnb_ipc_open",
     "rnnb_ipc_close", "rnnb_peer_access", "rnnb_flag_signal", "rnnb_flag_wait",
+    "rnnb_gemm", "rnnb_activation",
 )
 MAX_PEERS = 7
 IPC_HANDLE_BYTES = 64
@@ -85,6 +86,8 @@ def load():
         "rnnb_peer_access": ([ci, ci], ci),
         "rnnb_flag_signal": ([ci, vp, ctypes.c_uint32, vp], ci),
         "rnnb_flag_wait": ([ci, vp, ctypes.c_uint32, vp], ci),
+        "rnnb_gemm": ([ci, vp, i64, vp, i64, vp, i64, i64, i64, i64, ci, vp], ci),
+        "rnnb_activation": ([ci, vp, vp, i64, ci, vp], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
