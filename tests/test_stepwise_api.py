@@ -50,7 +50,7 @@ def test_step_chain_equals_layer_and_oracle(oracle, kind, dtype):
     if kind == "lstm":
         ref = oracle.lstm_stepwise(w, X)
     else:
-        ref = oracle.layer_stepwise(kind, mats, X)
+        ref = oracle.layer_stepwise(kind, mats, X)[0]
     tol = 1e-5 if dtype == np.float32 else 1e-12
     scale = max(float(np.max(np.abs(ref))), 1e-30)
     assert np.max(np.abs(chain - ref)) / scale <= tol
