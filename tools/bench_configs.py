@@ -52,11 +52,66 @@ def timed(fn, reps, flush):
     return sum(ts) / len(ts)
 
 
+def p2p_runs(reps, flush):
+    """The fused peer-memory partitions (p2p.py) on ONE GPU: G ranks emulated
+    as rank objects with their own streams sharing the device, so the
+    numbers show the protocol's overhead (flags, chunking, epilogue stores to
+    several destinations) against the unpartitioned run -- not multi-GPU
+    scaling, which needs G GPUs."""
+    from paper_1803_11389_b200 import p2p
+    from paper_1803_11389_b200.partition import layer_ranges
+    out = []
+    w = workloads.make("cfg4")
+    X = torch.from_numpy(w.X).cuda()
+    L = w.seq_len
+    fl = workloads.flops_per_step(w)
+    for mode in ("bf16",):
+        whole = P.DeviceStack(w.kind, w.layers, mode=mode)
+        ms = timed(lambda: whole.forward(X, 32), reps, flush)
+        out.append({"config": "cfg4", "mode": mode, "T_b": 32, "path": "unpartitioned DeviceStack", "G": 1,
+                    "ms": round(ms, 3), "steps_per_s": round(L / ms * 1e3, 1)})
+        print(out[-1], flush=True)
+        whole.close()
+        for G in (2, 4):
+            stages = []
+            for g, (lo, hi) in enumerate(layer_ranges(len(w.layers), G)):
+                st = P.DeviceStack(w.kind, w.layers[lo:hi], mode=mode)
+                stages.append(p2p.P2PPipelineStage(st, g, G, 4096, 32, slots=2))
+            for s_ in stages:
+                s_.connect_local(stages)
+            ms = timed(lambda: p2p.run_local_pipeline(stages, X, L), reps, flush)
+            out.append({"config": "cfg4", "mode": mode, "T_b": 32, "G": G, "chunk": 4096, "slots": 2,
+                        "path": "P2P layer pipeline, ranks emulated on one GPU", "ms": round(ms, 3),
+                        "steps_per_s": round(L / ms * 1e3, 1), "tflops": round(fl * L / ms / 1e9, 2)})
+            print(out[-1], flush=True)
+            for s_ in stages:
+                s_.stack.close()
+    del X
+    torch.cuda.empty_cache()
+    w = workloads.make("cfg5")
+    X = torch.from_numpy(w.X).cuda()
+    L = w.seq_len
+    for G in (1, 2):
+        ranks = [p2p.P2PBidirSRU(w.layers, w.layers_bwd, g, G, 64, "bf16", L) for g in range(G)]
+        for r in ranks:
+            r.connect_local(ranks)
+        ms = timed(lambda: p2p.run_local_bidir(ranks, X), reps, flush)
+        out.append({"config": "cfg5", "mode": "bf16", "T_b": 64, "G": G,
+                    "path": "P2P hidden sharding, all-gather in the epilogue, ranks emulated on one GPU",
+                    "ms": round(ms, 3), "steps_per_s": round(L / ms * 1e3, 1)})
+        print(out[-1], flush=True)
+        del ranks
+        torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--configs", default="cfg1,cfg2,cfg3,cfg4,cfg5")
     ap.add_argument("--out", default=os.path.join(REPO, "gpurun_out", "configs.json"))
+    ap.add_argument("--p2p", action="store_true",
+                    help="also time the fused peer-memory partitions with G ranks emulated on this one GPU")
     a = ap.parse_args()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     res = {}
@@ -106,6 +161,8 @@ def main():
         res[name]["wall_s"] = round(time.time() - t0, 1)
         del X
         torch.cuda.empty_cache()
+    if a.p2p:
+        res["p2p_emulated"] = p2p_runs(a.reps, flush)
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as f:
         json.dump(res, f, indent=1)
