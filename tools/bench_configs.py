@@ -6,8 +6,8 @@ Per config, mode and T_b: W=3 warm-up forwards, then `reps` forwards, each
 bracketed by CUDA events with a 256 MB L2 flush before it; steps/s = L /
 mean time.  cfg1-cfg4 run the blocked stack (DeviceStack; cfg3 adds the
 120->1024 projection and 1024->2000 logits), cfg5 runs the bidirectional
-wide SRU through partition.ShardedBidirSRU at world size 1 (all units on
-this GPU).  Outputs are not re-verified here (tests/ do that).
+wide SRU through the fused sharded stack p2p.P2PBidirSRU at G = 1 (all
+units on this GPU).  Outputs are not re-verified here (tests/ do that).
 """
 
 import argparse
@@ -23,7 +23,7 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
 import paper_1803_11389_b200 as P  # noqa: E402
-from paper_1803_11389_b200 import partition, workloads  # noqa: E402
+from paper_1803_11389_b200 import workloads  # noqa: E402
 from paper_1803_11389_b200.acoustic import AcousticSRU  # noqa: E402
 
 PLAN = {
@@ -115,7 +115,6 @@ def main():
     a = ap.parse_args()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     res = {}
-    pg = False
     for name in a.configs.split(","):
         t0 = time.time()
         w = workloads.make(name)
@@ -128,22 +127,18 @@ def main():
                 model = AcousticSRU(w.proj, w.layers, w.logits, mode=mode)
                 run = lambda T: model.forward(X, T)
             elif name == "cfg5":
-                if not pg:
-                    import socket
-                    import torch.distributed as dist
-                    s = socket.socket()
-                    s.bind(("127.0.0.1", 0))
-                    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-                    os.environ.setdefault("MASTER_PORT", str(s.getsockname()[1]))
-                    s.close()
-                    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
-                    pg = True
+                # the fused sharded stack (p2p.py) at G = 1: all units on this GPU,
+                # backward direction stored with a negative row stride (no flips)
+                from paper_1803_11389_b200 import p2p
                 models = {}
 
                 def run(T, mode=mode):
                     if T not in models:
-                        models[T] = partition.ShardedBidirSRU(
-                            w.layers, w.layers_bwd, 0, 1, partition.wide_sru_stage_factory(T, mode, 0))
+                        models.clear()
+                        torch.cuda.empty_cache()
+                        r = p2p.P2PBidirSRU(w.layers, w.layers_bwd, 0, 1, T, mode, L)
+                        r.connect_local([r])
+                        models[T] = r
                     return models[T].forward(X)
             else:
                 st = P.DeviceStack(w.kind, w.layers, mode=mode)
