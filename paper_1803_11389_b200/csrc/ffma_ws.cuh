@@ -17,6 +17,8 @@
 #pragma once
 #include <cuda.h>  // CUtensorMap (type only; encoded via the runtime's driver entry point)
 
+#include <type_traits>
+
 #include "ffma_layer.cuh"
 
 namespace rnnb {
@@ -440,6 +442,23 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
     const size_t w_tap = WSTR ? w_chunk : (size_t)(Dp / KV) * Rs * KV;
     const size_t stage_tw = stage_bytes / sizeof(TW);
     const int kv_last = (Dp - (nchunk - 1) * KC) / KV;    // k-vectors in the last chunk
+    // One-column fp32 passes (T_b = 1) are bound by shared-memory bandwidth:
+    // every weight is re-read for one FMA.  Each lane keeps its weights of
+    // chunk 0 (TAPS x RH vectors = 88 registers at U = 7) in registers for the
+    // whole sequence and reads only the other chunks from shared memory
+    // (cfg2 T_b = 1: 0.87 -> 0.93 M steps/s; at NT = 2 the extra registers
+    // cost more than they save: 1.52 -> 1.33, so NT = 1 only).
+    constexpr bool kRegW = sizeof(TA) == 4 && sizeof(TW) == 4 && XR == XR_NONE && !WSTR && NT == 1;
+    ulonglong2 wreg[kRegW ? TAPS : 1][kRegW ? RH : 1];
+    if constexpr (kRegW) {
+      const bool has0 = nchunk > 1 || kl < kv_last;  // chunk 0 is partial only when it is the only chunk
+#pragma unroll
+      for (int tap = 0; tap < TAPS; ++tap)
+#pragma unroll
+        for (int r = 0; r < RH; ++r)
+          wreg[tap][r] = has0 ? *reinterpret_cast<const ulonglong2*>(wlane_base + (size_t)tap * w_tap + r * KV)
+                              : make_ulonglong2(0ull, 0ull);
+    }
     uint32_t seq = 0, pass = 0;
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
@@ -484,16 +503,22 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
 #pragma unroll
                 for (int ct = 0; ct < CT; ++ct)
                   xp[ct] = *reinterpret_cast<const ulonglong2*>(xl + (size_t)(LANES_T * ct - tap) * BXS);
+                auto rows = [&](auto from_regs) {
 #pragma unroll
-                for (int r = 0; r < RH; ++r) {
-                  const ulonglong2 w = *reinterpret_cast<const ulonglong2*>(wp + r * KV);
-                  // both k-pair halves of a row: CT independent FFMA2 between
-                  // the two updates of one accumulator
+                  for (int r = 0; r < RH; ++r) {
+                    ulonglong2 w;
+                    if constexpr (decltype(from_regs)::value) w = wreg[kRegW ? tap : 0][kRegW ? r : 0];
+                    else w = *reinterpret_cast<const ulonglong2*>(wp + r * KV);
+                    // both k-pair halves of a row: CT independent FFMA2 between
+                    // the two updates of one accumulator
 #pragma unroll
-                  for (int ct = 0; ct < CT; ++ct) acc2[r][ct] = ffma2_sel<C::CTW == 4>(w.x, xp[ct].x, acc2[r][ct]);
+                    for (int ct = 0; ct < CT; ++ct) acc2[r][ct] = ffma2_sel<C::CTW == 4>(w.x, xp[ct].x, acc2[r][ct]);
 #pragma unroll
-                  for (int ct = 0; ct < CT; ++ct) acc2[r][ct] = ffma2_sel<C::CTW == 4>(w.y, xp[ct].y, acc2[r][ct]);
-                }
+                    for (int ct = 0; ct < CT; ++ct) acc2[r][ct] = ffma2_sel<C::CTW == 4>(w.y, xp[ct].y, acc2[r][ct]);
+                  }
+                };
+                if (kRegW && ccur == 0) rows(std::integral_constant<bool, kRegW>{});
+                else rows(std::false_type{});
               } else {
                 TA xv[CT][KV];
 #pragma unroll
