@@ -188,10 +188,50 @@ struct WsCfg {
   // WSTR: weights are not resident, so the ring can be deeper; each stage
   // also carries the chunk's weight image
   static constexpr int STAGES = WSTR ? 6 : (NT == 32 ? 3 : 4);
-  // reduce-scatter over the LANES_K lanes of a k-group: NV partials per lane
-  // (padded to a multiple of LANES_K), NV / LANES_K sums per lane afterwards
-  static constexpr int NV = (RH * CT + LANES_K - 1) / LANES_K * LANES_K;
 };
+
+// Reduce-scatter of NR partials over the lanes whose bits are O, 2O, .., 16:
+// at each level a lane keeps the half of its live partials selected by its
+// lane bit and adds the partner's copy of that half, so partial j ends in one
+// lane; odd counts are padded by one zero (not the old padding of NR up to a
+// multiple of the lane count: at NT = 1, 11 partials over 32 lanes cost 13
+// shuffles instead of 31).  Once one partial is left, the remaining levels
+// are a butterfly: both partners hold the sum and the upper one is marked
+// `dup`.  Afterwards a lane holds partials jb .. jb + ws_rs_final - 1, of
+// which the first `nreal` are real (the rest are padding: with odd counts
+// a padded slot's index can coincide with a real partial of another lane).
+template <int CUR, int O>
+__host__ __device__ constexpr int ws_rs_final() {
+  if constexpr (O >= 32) return CUR;
+  else return ws_rs_final<(CUR > 1 ? (CUR + 1) / 2 : 1), O * 2>();
+}
+template <typename TA, int CUR, int O, int N>
+__device__ __forceinline__ void ws_reduce_scatter(TA (&v)[N], int lane, int& jb, bool& dup, int& nreal) {
+  if constexpr (O < 32) {
+    const bool upper = (lane & O) != 0;
+    if constexpr (CUR > 1) {
+      constexpr int HALF = (CUR + 1) / 2;
+#pragma unroll
+      for (int i = 0; i < HALF; ++i) {
+        const TA hi = (i + HALF < CUR) ? v[i + HALF] : TA(0);
+        const TA send = upper ? v[i] : hi;
+        const TA keep = upper ? hi : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+      }
+      if (upper) {
+        jb += HALF;
+        nreal = nreal > HALF ? nreal - HALF : 0;
+      } else {
+        nreal = nreal < HALF ? nreal : HALF;
+      }
+      ws_reduce_scatter<TA, HALF, O * 2>(v, lane, jb, dup, nreal);
+    } else {
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], O);
+      if (upper) dup = true;
+      ws_reduce_scatter<TA, 1, O * 2>(v, lane, jb, dup, nreal);
+    }
+  }
+}
 
 // x chunk of KC columns = KC/BW TMA boxes of [NT+1 rows x (BW + PADV) cols],
 // each box at a 128-byte aligned stride inside the stage buffer
@@ -549,35 +589,44 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
             for (int ct = 0; ct < CT; ++ct)
               acc[r][ct] = __uint_as_float((unsigned)acc2[r][ct]) + __uint_as_float((unsigned)(acc2[r][ct] >> 32));
         }
-        // reduce-scatter over the LANES_K lanes of the k-group: at each level a
-        // lane keeps the half of its live partials selected by its lane bit
-        // and adds the partner's copy, so partial j ends in one lane only
-        constexpr int NV = C::NV;
+        // reduce-scatter over the LANES_K lanes of the k-group.  Short passes
+        // (NT <= 4: 32 lanes split K, few partials) use the minimal-padding
+        // ws_reduce_scatter; wider passes pad the partials to a multiple of
+        // LANES_K (little padding there, and it fits the 168-register budget)
+        constexpr int NR = RH * CT;
+        constexpr bool kMinPad = NT <= 4;
+        constexpr int NV = kMinPad ? NR : (NR + LANES_K - 1) / LANES_K * LANES_K;
         TA v[NV];
 #pragma unroll
-        for (int j = 0; j < NV; ++j) v[j] = j < RH * CT ? acc[j / CT][j % CT] : TA(0);
+        for (int j = 0; j < NV; ++j) v[j] = j < NR ? acc[j / CT][j % CT] : TA(0);
+        int jb = 0, nreal = NV;
+        bool dup = false;
+        if constexpr (kMinPad) {
+          ws_reduce_scatter<TA, NR, LANES_T>(v, lane, jb, dup, nreal);
+        } else {
 #pragma unroll
-        for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) {
-          const bool upper = (lane & o) != 0;
+          for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) {
+            const bool upper = (lane & o) != 0;
 #pragma unroll
-          for (int i = 0; i < ns; ++i) {
-            const TA send = upper ? v[i] : v[i + ns];
-            const TA keep = upper ? v[i + ns] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            for (int i = 0; i < ns; ++i) {
+              const TA send = upper ? v[i] : v[i + ns];
+              const TA keep = upper ? v[i + ns] : v[i];
+              v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+            }
           }
-        }
-        // lane bits (LANES_T, 2 LANES_T, ...) chose offsets (NV/2, NV/4, ...)
-        int jb = 0;
+          // lane bits (LANES_T, 2 LANES_T, ...) chose offsets (NV/2, NV/4, ...)
 #pragma unroll
-        for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) jb += (lane & o) ? ns : 0;
+          for (int o = LANES_T, ns = NV / 2; o < 32; o <<= 1, ns >>= 1) jb += (lane & o) ? ns : 0;
+        }
+        constexpr int NF = kMinPad ? ws_rs_final<NR, LANES_T>() : NV / LANES_K;
         const int rb = NRED == 2 ? (int)(pass & 1) : 0;
         const uint32_t rph = (NRED == 2 ? pass >> 1 : pass) & 1;
         TA* redb = red + rb * red_elems;
         mbar_wait(&redempty[rb], rph ^ 1);
 #pragma unroll
-        for (int i = 0; i < NV / LANES_K; ++i) {
+        for (int i = 0; i < NF; ++i) {
           const int j = jb + i;
-          if (j < RH * CT) {
+          if (!dup && i < nreal && j < NR) {
             const int r = j / CT, ct = j - (j / CT) * CT;
             redb[((size_t)kg * Rpad + rbase + r) * NT + tq + LANES_T * ct] = v[i];
           }
