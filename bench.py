@@ -137,8 +137,9 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
         fp = os.path.join(REPO, "profiles", "ffma_peak.json")
         if os.path.exists(fp):
             with open(fp) as f:
-                peak = json.load(f)["reg3_tflops"]
-            src = "measured: tools/ffma_peak.cu register FFMA, profiles/ffma_peak.json"
+                peak = json.load(f)["fma_peak_tflops"]
+            src = ("measured: tools/ffma_peak2.cu packed FFMA2, 32 independent chains, profiles/ffma_peak.json "
+                   "(0.96 of nominal)")
         else:
             peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
             src = f"nominal: 148 SMs x 128 lanes x 2 FLOP x {mhz:.0f} MHz"

@@ -23,6 +23,9 @@
 
 namespace rnnb {
 
+#ifndef RNNB_PROD_SLEEP_NS
+#define RNNB_PROD_SLEEP_NS 1024  // producer back-off cap while waiting for a free ring slot
+#endif
 #ifndef RNNB_WIDE_MIN_NT
 #define RNNB_WIDE_MIN_NT 1
 #endif
@@ -359,7 +362,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
           const int s = seq % STAGES;
           const uint32_t ph = (seq / STAGES) & 1;
           if (a.dbg & 1) continue;
-          mbar_wait_sleep(&empty[s], ph ^ 1);
+          mbar_wait_sleep(&empty[s], ph ^ 1, RNNB_PROD_SLEEP_NS);
           if constexpr (STREAM) {
             if (ch == 0 && !timed_out)
               timed_out = !wait_rows(a.x_ready, (int)((tp + NT) < a.L ? (tp + NT) : a.L), t_start, a.stream_fail);
