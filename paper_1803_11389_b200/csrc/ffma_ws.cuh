@@ -29,7 +29,10 @@ namespace rnnb {
 #ifndef RNNB_WIDE_MIN_NT
 #define RNNB_WIDE_MIN_NT 1
 #endif
-constexpr int kWsEpiWarps = 2;
+#ifndef RNNB_EPI_WARPS
+#define RNNB_EPI_WARPS 2
+#endif
+constexpr int kWsEpiWarps = RNNB_EPI_WARPS;
 constexpr int kWsEpiThreads = kWsEpiWarps * 32;
 
 // named barrier 1 over the epilogue warpgroup only
