@@ -359,6 +359,139 @@ def run_ours(args, rank, world, local_rank):
 
 
 # ---------------------------------------------------------------------------
+# partitioned configs across ranks: the fused peer-memory partitions (p2p.py)
+
+
+def run_partitioned(args, rank, world, local_rank):
+    """BASELINE cfg4 (--partition pipeline: layer pipeline of time chunks) or
+    cfg5 (--partition hidden: hidden-dimension sharding with the all-gather
+    in the epilogue) over the ranks, one GPU each (CUDA IPC between the rank
+    processes; BENCH_SHARE_GPU=1 puts every rank on cuda:0 to exercise the
+    path).  Strong scaling: the whole sequence per step, time = max over
+    ranks of the device time per step."""
+    import torch
+    import torch.distributed as dist
+    import paper_1803_11389_b200 as P
+    from paper_1803_11389_b200 import p2p
+    from paper_1803_11389_b200.partition import layer_ranges
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    w = workloads.make(args.workload)
+    L = w.seq_len
+    last = rank == world - 1
+    if args.partition == "pipeline":
+        if w.bidirectional or w.proj is not None:
+            raise SystemExit("--partition pipeline needs a plain stack (cfg4)")
+        lo, hi = layer_ranges(len(w.layers), world)[rank]
+        st = P.DeviceStack(w.kind, w.layers[lo:hi], mode=args.mode, device=local_rank)
+        obj = p2p.P2PPipelineStage(st, rank, world, args.chunk, args.block, slots=2)
+        X = torch.from_numpy(w.X).to(dev) if rank == 0 else None
+        out = torch.empty((L, st.d_h[-1]), dtype=torch.float32, device=dev) if last else None
+        d_in, d_out = int(w.X.shape[1]), int(w.layers[-1].d_h)
+
+        def step():
+            obj.enqueue(L, X, out)
+            obj.advance(L)
+            obj.finish()
+        par = f"pipeline{world} (layers {lo}..{hi - 1} on rank {rank}, chunk {args.chunk})"
+    else:
+        if not w.bidirectional:
+            raise SystemExit("--partition hidden needs the bidirectional stack (cfg5)")
+        obj = p2p.P2PBidirSRU(w.layers, w.layers_bwd, rank, world, args.block, args.mode, L, device=local_rank)
+        X = torch.from_numpy(w.X).to(dev)
+        out = torch.empty((L, 2 * obj.H), dtype=torch.float32, device=dev)
+        d_in, d_out = int(w.X.shape[1]), 2 * obj.H
+
+        def step():
+            obj.enqueue(X, out)
+            obj.close_call()
+            torch.cuda.current_stream(dev).wait_stream(obj.stream)
+        par = f"hidden{world} (units {obj.u0}..{obj.u1 - 1} of each direction on rank {rank})"
+    if world > 1:
+        obj.connect_ipc()
+    else:
+        obj.connect_local([obj])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        ev[i][0].record()
+        step()
+        ev[i][1].record()
+    while not ev[-1][1].query():
+        time.sleep(0.0005)
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    ms = sum(a.elapsed_time(b) for a, b in ev) / args.steps
+    # end to end: rank 0 copies the sequence in from pinned host memory, the
+    # ranks holding the output copy it out; wall clock, max over ranks
+    Xh = torch.from_numpy(w.X).pin_memory() if X is not None else None
+    Oh = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() if out is not None else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e_steps = max(3, min(args.steps, 10))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        if Xh is not None:
+            X.copy_(Xh, non_blocking=True)
+        step()
+        if Oh is not None and (last if args.partition == "pipeline" else rank == 0):
+            Oh.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / e_steps
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = float(t[0]), float(t[1])
+    # this rank's kernel launches per step (layer kernels + operand copies + flag signals)
+    if args.partition == "pipeline":
+        n_chunks = -(-L // args.chunk)
+        launches = n_chunks * (obj.stack.last_launches + (rank < world - 1) + (rank > 0))
+    else:
+        per_dir = [st_.last_launches for st_ in obj.stages[-1]]
+        launches = len(obj.stages) * (sum(per_dir) + 1 + world) + 1
+    obj.close()
+    if rank != 0:
+        return None
+    pk, pk_src = peaks()
+    flops = workloads.flops_per_step(w) * L
+    tc = args.mode in ("bf16", "tf32")
+    peak = (pk["bf16_tflops"] * (0.5 if args.mode == "tf32" else 1.0)) if tc else 71.29
+    achieved = flops / (ms / 1e3) / 1e12
+    itemsize = 4
+    return {
+        "metric": METRIC, "value": round(L / (ms / 1e3), 1), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.mode,
+        "data": "synthetic (seeded PCG64, BASELINE.json distributions)",
+        "config": {"workload": args.workload, "seq_len": L, "block_size": args.block, "mode": args.mode,
+                   "parallelism": par, "transport": "fused epilogue stores to CUDA-IPC-mapped peer buffers + "
+                   "stream-ordered flags" if world > 1 else "single rank (no peers)",
+                   "l2": "flushed before every timed step (256 MB write)"},
+        "e2e": {"value": round(L / (e2e_ms / 1e3), 1), "unit": UNIT,
+                "h2d_bytes_per_step": int(L * d_in * itemsize),
+                "d2h_bytes_per_step": int(L * d_out * itemsize),
+                "ms_per_step": round(e2e_ms, 4), "api": "p2p partition objects, pinned host X / output"},
+        "gpu_launches": int(launches * args.steps),
+        "roofline": {"bound": "tensor" if tc else "compute", "achieved": round(achieved, 2),
+                     "peak": round(peak * world, 1), "unit": "TFLOP/s", "frac": round(achieved / (peak * world), 4),
+                     "peak_source": ("MEASURED_PEAKS.json" if tc else "profiles/ffma_peak.json") + f" x {world} GPUs",
+                     "traffic": None},
+        "clocks": clocks,
+    }
+
+
+# ---------------------------------------------------------------------------
 # reference arm / cpu baseline: the oracle port of rnnblock's fast path
 
 
@@ -436,6 +569,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-sample", type=int, default=512, help="time steps in the CPU sample")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--partition", choices=("replicas", "pipeline", "hidden"), default="replicas",
+                    help="replicas: N independent copies of the workload (cfg1/cfg2 do not shard); "
+                         "pipeline: cfg4 layer pipeline across ranks; hidden: cfg5 hidden sharding")
+    ap.add_argument("--chunk", type=int, default=4096, help="pipeline chunk (steps, a multiple of --block)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: W < 3 warm-up steps violates the timing rules; using 3")
@@ -461,7 +598,10 @@ def main():
                 dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
             else:
                 dist.init_process_group(backend)
-        line = run_ours(args, rank, world, local_rank)
+        if args.partition == "replicas":
+            line = run_ours(args, rank, world, local_rank)
+        else:
+            line = run_partitioned(args, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()
