@@ -746,34 +746,46 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
       !g_stream_disabled && !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
   StreamOps so = stream_ops();
   if (want_stream && so.write && so.wait) {
-    // chunk: whole blocks, >= kMinChunk steps (RNNB_STREAM_CHUNK), at most
-    // kMaxStreamChunks of them; small chunks shorten the exposed first
-    // copy-in and last copy-out
+    // The kernel counts finished h rows per granule g (whole blocks, >= 32
+    // steps, at most kMaxStreamChunks granules).  Copies move segments of
+    // whole granules: the first and the last segment are one granule (short
+    // exposed copy-in before the first pass and copy-out after the last),
+    // the others ~RNNB_STREAM_CHUNK steps (fewer, larger copies).
     const char* env_c = getenv("RNNB_STREAM_CHUNK");
     const int64_t min_chunk = env_c ? atoll(env_c) : 128;  // measured cfg2 (32-column passes): 64 -> 2.17-2.42M (noisy), 128 -> 2.64M, 256 -> 2.56M e2e
-    int64_t sc = (L + kMaxStreamChunks - 1) / kMaxStreamChunks;
-    if (sc < min_chunk) sc = min_chunk;
-    if (sc < 1) sc = 1;
-    sc = (sc + T - 1) / T * T;
-    const int64_t nsc = (L + sc - 1) / sc;
-    if (nsc <= kMaxStreamChunks) {
+    int64_t g = (32 + T - 1) / T * T;
+    const int64_t gmin = (L + kMaxStreamChunks - 1) / kMaxStreamChunks;
+    if (g < gmin) g = (gmin + T - 1) / T * T;
+    const int64_t ng = (L + g - 1) / g;
+    int64_t sc = (min_chunk + g - 1) / g * g;
+    if (sc < g) sc = g;
+    std::vector<int64_t> seg{0};  // segment boundaries (multiples of g, then L)
+    const int64_t last0 = (L - 1) / g * g;  // start of the last granule
+    if (last0 > 0) {
+      seg.push_back(g);
+      for (int64_t t = g + sc; t < last0; t += sc) seg.push_back(t);
+      if (seg.back() < last0) seg.push_back(last0);
+    }
+    seg.push_back(L);
+    const int64_t nsc = (int64_t)seg.size() - 1;
+    if (ng <= kMaxStreamChunks) {
       if (!h->stream_ctr) {
         CUDA_TRY(cudaMalloc(&h->stream_ctr, (2 + kMaxStreamChunks) * sizeof(int)));
         CUDA_TRY(cudaHostAlloc(&h->stream_flag_host, sizeof(int), cudaHostAllocDefault));
       }
-      CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (2 + nsc) * sizeof(int), s));
+      CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (2 + ng) * sizeof(int), s));
       CUDA_TRY(cudaEventRecord(ev_start, s));
       CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
       CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
       h->stream_ready = h->stream_ctr;
       h->stream_done = h->stream_ctr + 2;
-      h->stream_chunk = (int)sc;
+      h->stream_chunk = (int)g;
       h->stream_refused = false;
-      // chunk 0's copy-in first: its rows land while the layer kernel is
+      // segment 0's copy-in first: its rows land while the layer kernel is
       // still being launched and loads its weights (the kernel polls the
       // counter); if the layer cannot stream, the chunked path below copies again
       auto copy_in = [&](int64_t i) -> rnnb_status {
-        const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
+        const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
         CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice,
                                  h->s_in));
         CU_TRY(so.write(h->s_in, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
@@ -788,8 +800,11 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
         for (int64_t i = 1; i < nsc; ++i)
           if ((st = copy_in(i)) != RNNB_OK) return st;
         for (int64_t i = 0; i < nsc; ++i) {
-          const int64_t t0 = i * sc, n = (L - t0) < sc ? (L - t0) : sc;
-          CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 2 + i), grid, CU_STREAM_WAIT_VALUE_GEQ));
+          // every CTA finished the segment's last granule => all of the
+          // segment (a CTA stores its passes in order)
+          const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
+          CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 2 + (seg[i + 1] - 1) / g), grid,
+                         CU_STREAM_WAIT_VALUE_GEQ));
           CUDA_TRY(cudaMemcpyAsync(hH + t0 * dh * es, dH + t0 * dh * es, n * dh * es, cudaMemcpyDeviceToHost,
                                    h->s_out));
         }
