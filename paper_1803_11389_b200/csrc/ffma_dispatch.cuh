@@ -156,7 +156,10 @@ static bool reg_eligible(const LayerArgs<TA, TW>& a) {
     if ((a.ldx % 4) != 0 || !al(a.X) || (a.xcarry != nullptr && !al(a.xcarry))) return false;
     const char* env = getenv("RNNB_REG");
     if (env) return env[0] == '1';
-    return a.T_b <= 2;  // measured crossover (cfg1: 2.77 M flat vs SMEM kernel 1.26 / 1.81 / 3.17 M at T_b 1/2/4)
+    // measured crossover: T_b = 1 only since the shared-memory kernel's short
+    // passes got cheaper (cfg1 T_b=2: 2.13 reg vs 2.26 M steps/s ws; cfg3:
+    // 0.302 vs 0.326 M; at T_b=1 reg still wins: cfg1 2.13 vs 1.53, cfg3 0.302 vs 0.180)
+    return a.T_b <= 1;
   }
 }
 
