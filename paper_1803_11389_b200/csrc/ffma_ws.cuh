@@ -29,15 +29,24 @@ namespace rnnb {
 #ifndef RNNB_WIDE_MIN_NT
 #define RNNB_WIDE_MIN_NT 1
 #endif
-#ifndef RNNB_EPI_WARPS
-#define RNNB_EPI_WARPS 2
+#ifndef RNNB_NT32_NRED
+#define RNNB_NT32_NRED 1  // 32-column passes: double-buffered cross-warp partials (1) or single (0)
 #endif
-constexpr int kWsEpiWarps = RNNB_EPI_WARPS;
-constexpr int kWsEpiThreads = kWsEpiWarps * 32;
+#ifndef RNNB_NT32_STAGES
+#define RNNB_NT32_STAGES 3
+#endif
+// Epilogue warps: 3 beside the 8 consumer warps of the wide fp32 tile (the
+// epilogue competes with the consumers for issue slots and falls behind with
+// 2: 3 measured +1.4 % at T_b=32, +2.5 % at T_b=8; 1 -> -3 %; 4 lowers the
+// register cap to 152 -> spills); 2 beside 16 consumer warps (96-register cap).
+#ifndef RNNB_EPI_WARPS
+#define RNNB_EPI_WARPS 3
+#endif
 
 // named barrier 1 over the epilogue warpgroup only
+template <int NTHR>
 __device__ __forceinline__ void epi_bar_sync() {
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kWsEpiThreads) : "memory");
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NTHR) : "memory");
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -172,7 +181,9 @@ struct WsCfg {
   static constexpr int RG = R > 24 ? 4 : 2;
   static constexpr int KG = (CTW == 4 ? 8 : 16) / RG;
   static constexpr int CW = KG * RG;                       // consumer warps
-  static constexpr int THREADS = (CW + 1 + kWsEpiWarps) * 32;  // + producer + epilogue group
+  static constexpr int EPIW = CW == 8 ? RNNB_EPI_WARPS : 2;  // epilogue warps
+  static constexpr int EPIT = EPIW * 32;
+  static constexpr int THREADS = (CW + 1 + EPIW) * 32;  // + producer + epilogue group
   static constexpr int RH = (R + RG - 1) / RG;
   static constexpr int Rpad = RH * RG;
   // smem row count per k-vector: odd so consecutive kv (lanes kq) hit distinct
@@ -190,10 +201,10 @@ struct WsCfg {
   // pays for the second buffer with one x stage
   // (also the short fp32 passes, NT <= 8, where a pass lasts ~1 us and the
   // buffers cost < 3 KB)
-  static constexpr int NRED = (NT == 32 || (sizeof(TA) == 4 && NT <= 8)) ? 2 : 1;
+  static constexpr int NRED = (NT == 32 ? RNNB_NT32_NRED : (sizeof(TA) == 4 && NT <= 8)) ? 2 : 1;
   // WSTR: weights are not resident, so the ring can be deeper; each stage
   // also carries the chunk's weight image
-  static constexpr int STAGES = WSTR ? 6 : (NT == 32 ? 3 : 4);
+  static constexpr int STAGES = WSTR ? 6 : (NT == 32 ? RNNB_NT32_STAGES : 4);
 };
 
 // Reduce-scatter of NR partials over the lanes whose bits are O, 2O, .., 16:
@@ -411,7 +422,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
     }
   } else if (warp > CW) {
     // ------------- epilogue warpgroup: sums, activations, scan, output -------------
-    const int et = tid - (CW + 1) * 32;  // 0 .. kWsEpiThreads-1
+    const int et = tid - (CW + 1) * 32;  // 0 .. EPIT-1
     TA c = TA(0);
     if (et < U && a.c_in != nullptr && u0 + et < a.H) c = a.c_in[u0 + et];
     uint32_t pass = 0;
@@ -424,7 +435,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
         const uint32_t rph = (NRED == 2 ? pass >> 1 : pass) & 1;
         const TA* redb = red + rb * red_elems;
         mbar_wait_sleep(&redfull[rb], rph, NT <= 8 ? 128u : 1024u);  // short passes: wake promptly
-        for (int i = et; i < ((a.dbg & 4) ? 0 : R * nt); i += kWsEpiThreads) {
+        for (int i = et; i < ((a.dbg & 4) ? 0 : R * nt); i += C::EPIT) {
           const int r = i / nt, col = i - (i / nt) * nt;
           TA s = TA(0);
 #pragma unroll
@@ -436,7 +447,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
           else v = g == 0 ? tanh_full(s) : sigmoid_ref<TA>(s);
           gate[((size_t)g * U + u) * NT + col] = v;
         }
-        epi_bar_sync();
+        epi_bar_sync<C::EPIT>();
         if (et == 0) mbar_arrive(&redempty[rb]);
         if (et < U && !(a.dbg & 4)) {
           TA* cand = gate + (size_t)et * NT;
@@ -447,8 +458,8 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
             cand[col] = c;
           }
         }
-        epi_bar_sync();
-        for (int i = et; i < ((a.dbg & 4) ? 0 : U * nt); i += kWsEpiThreads) {
+        epi_bar_sync<C::EPIT>();
+        for (int i = et; i < ((a.dbg & 4) ? 0 : U * nt); i += C::EPIT) {
           const int u = i % U, col = i / U;
           const int unit = u0 + u;
           if (unit < a.H) {
@@ -459,7 +470,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
             store_h(a, (tp + col) * a.ldh + unit, h);
           }
         }
-        epi_bar_sync();
+        epi_bar_sync<C::EPIT>();
         if constexpr (STREAM) {
           if (et == 0 && ((tp + nt) % a.h_chunk == 0 || tp + nt == a.L)) {
             __threadfence();  // this CTA's h rows of the chunk (ordered by the barrier) before the count
