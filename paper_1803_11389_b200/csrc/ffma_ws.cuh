@@ -132,27 +132,27 @@ __device__ __forceinline__ unsigned long long ffma2_sel(unsigned long long a, un
 // host sees the flag and recomputes without streaming.  Returns false on
 // time-out.
 constexpr uint64_t kStreamTimeoutNs = 2000000000ull;
-__device__ __forceinline__ bool wait_rows(const int* ready, int need, uint64_t t_start, int* fail) {
-  int ok = 1;
+__device__ __forceinline__ int wait_rows(const int* ready, int need, uint64_t t_start, int* fail) {
+  // returns the row count observed (>= need), or -1 after the time-out
+  int have = 0;
   if ((threadIdx.x & 31) == 0) {
-    uint32_t ns = 64;
+    uint32_t ns = 32;
     while (true) {
-      int v;
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ready) : "memory");
-      if (v >= need) break;
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(have) : "l"(ready) : "memory");
+      if (have >= need) break;
       uint64_t now;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
       if (now - t_start > kStreamTimeoutNs) {
         atomicExch(fail, 1);
-        ok = 0;
+        have = -1;
         break;
       }
       __nanosleep(ns);
-      ns = ns < 2048 ? ns * 2 : 2048;
+      ns = ns < 256 ? ns * 2 : 256;
     }
     asm volatile("fence.proxy.async.global;" ::: "memory");
   }
-  return __shfl_sync(0xffffffffu, ok, 0) != 0;
+  return __shfl_sync(0xffffffffu, have, 0);
 }
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -366,6 +366,7 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
     uint32_t seq = 0;
     bool timed_out = false;
     uint64_t t_start = 0;
+    int rows_seen = 0;  // STREAM: rows of X known to be resident
     if constexpr (STREAM) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     for (int64_t t0 = 0; t0 < a.L; t0 += a.T_b) {
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
@@ -378,8 +379,13 @@ __global__ void __launch_bounds__(WsCfg<TA, TW, CELL, NT, U, WSTR>::THREADS, 1)
           if (a.dbg & 1) continue;
           mbar_wait_sleep(&empty[s], ph ^ 1, RNNB_PROD_SLEEP_NS);
           if constexpr (STREAM) {
-            if (ch == 0 && !timed_out)
-              timed_out = !wait_rows(a.x_ready, (int)((tp + NT) < a.L ? (tp + NT) : a.L), t_start, a.stream_fail);
+            // rows already seen resident need no new acquire round trip
+            const int need = (int)((tp + NT) < a.L ? (tp + NT) : a.L);
+            if (ch == 0 && !timed_out && need > rows_seen) {
+              const int got = wait_rows(a.x_ready, need, t_start, a.stream_fail);
+              if (got < 0) timed_out = true;
+              else rows_seen = got;
+            }
           }
           const int d0 = ((ch + rot) % nchunk) * KC;  // per-CTA chunk rotation spreads L2 hot lines
           const int kcs = (Dp - d0) < KC ? (Dp - d0) : KC;
