@@ -61,7 +61,8 @@ typedef enum { RNNB_SRU = 1, RNNB_QRNN = 2 } rnnb_cell;
  * TF32 rounds weights and x to tf32 at the product (fp32 accumulate).
  * F32X3: fp32 inputs, products split 3xTF32 on the tensor cores
  * (a_hi b_hi + a_hi b_lo + a_lo b_hi), accumulated in 128-deep K chunks whose
- * partials are summed in fp32, for 16 <= T_b <= 32; fp32 FFMA otherwise. */
+ * partials are summed in fp32, for T_b >= 16 (longer blocks run as 32-step
+ * tensor-core blocks); fp32 FFMA below 16. */
 typedef enum { RNNB_F32 = 0, RNNB_F64 = 1, RNNB_BF16 = 2, RNNB_TF32 = 3, RNNB_F32X3 = 4 } rnnb_mode;
 
 typedef enum { RNNB_DT_F32 = 0, RNNB_DT_F64 = 1 } rnnb_dtype;

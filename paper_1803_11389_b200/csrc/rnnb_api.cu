@@ -204,7 +204,12 @@ bool use_tc(const rnnb_stack* h, int64_t Tb) {
   // steps/s), tf32 from T_b = 2 (1.29 vs 0.95)
   const int lo = mn ? atoi(mn) : (h->mode == RNNB_BF16 ? 1 : 2);
   if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32) return Tb >= lo && Tb <= 128;
-  if (h->mode == RNNB_F32X3) return Tb >= 16 && Tb <= 32;
+  // f32x3: T_b >= 16 (below, the exact FFMA kernel is faster); blocks longer
+  // than 32 steps run as 32-step tensor-core blocks (the 3N chunk partials
+  // live in registers: N <= 32), i.e. each weight is read into the tensor
+  // pipe once per 32 steps -- the same cap as the FFMA kernel's 32-column
+  // passes (cfg2 T_b=64: 2.9 M steps/s on the FFMA fallback before)
+  if (h->mode == RNNB_F32X3) return Tb >= 16;
   return false;
 }
 
@@ -213,10 +218,11 @@ int tc_mode_of(int mode) {
 }
 
 // one layer on the tcgen05 path (tc_layer.cuh)
-rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb, float* Hout,
-                            int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
+rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb_req,
+                            float* Hout, int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
   Layer& ly = h->layers[li];
   const int mode = tc_mode_of(h->mode);
+  const int64_t Tb = (mode == TC_3XTF32 && Tb_req > 32) ? 32 : Tb_req;  // see use_tc
   const int es = mode == TC_BF16 ? 2 : 4;
   const int64_t ldop = (ly.din + 7) / 8 * 8;
   const size_t opb = (size_t)(mode == TC_3XTF32 ? 2 : 1) * (L + 1) * ldop * es;

@@ -411,16 +411,17 @@ def test_tensor_core_look_back_is_deterministic(P, oracle):
 
 @pytest.mark.parametrize("kind", ["sru", "qrnn"])
 def test_f32x3_split_tensor_core_meets_fp32_bound(P, oracle, kind):
-    """3xTF32 split products on tcgen05 (mode "f32x3", 16 <= T_b <= 32) with
-    128-deep K chunks summed in fp32 meet the fp32 bound (normwise 1e-5,
-    max-abs 1e-4); the error vs an f64 oracle is reported beside FFMA's."""
+    """3xTF32 split products on tcgen05 (mode "f32x3", T_b >= 16; blocks past
+    32 steps run as 32-step tensor-core blocks) with 128-deep K chunks summed
+    in fp32 meet the fp32 bound (normwise 1e-5, max-abs 1e-4); the error vs
+    an f64 oracle is reported beside FFMA's."""
     import torch
     d = 512
     layers = oracle.generate_layers(kind, d, d, 2, 51, np.float32)
     X = np.random.default_rng(12).standard_normal((600, d)).astype(np.float32)
     st = P.DeviceStack(kind, layers, mode="f32x3")
     ref64 = oracle.run_blocked(kind, [[m.astype(np.float64) for m in l] for l in layers], X.astype(np.float64), 32)
-    for T in (16, 24, 32):
+    for T in (64, 48, 16, 24, 32):
         H = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
         assert st.query(9) == 1
         ref = oracle.run_blocked(kind, layers, X, T)
