@@ -65,7 +65,7 @@ typedef enum { RNNB_SRU = 1, RNNB_QRNN = 2 } rnnb_cell;
  * tensor-core blocks); fp32 FFMA below 16. */
 typedef enum { RNNB_F32 = 0, RNNB_F64 = 1, RNNB_BF16 = 2, RNNB_TF32 = 3, RNNB_F32X3 = 4 } rnnb_mode;
 
-typedef enum { RNNB_DT_F32 = 0, RNNB_DT_F64 = 1 } rnnb_dtype;
+typedef enum { RNNB_DT_F32 = 0, RNNB_DT_F64 = 1, RNNB_DT_U64 = 2 } rnnb_dtype;
 
 typedef struct rnnb_stack* rnnb_stack_t;
 
@@ -147,6 +147,15 @@ rnnb_status rnnb_finalize(int kind, const void* out_gate, const void* C, const v
 rnnb_status rnnb_gemm(int strict, const void* A, int64_t lda, const void* B, int64_t ldb, void* C,
                       int64_t ldc, int64_t m, int64_t n, int64_t k, int dtype, void* stream);
 rnnb_status rnnb_activation(int which, const void* x, void* y, int64_t n, int dtype, void* stream);
+
+/* Deterministic parameters of the reference's generators on the device:
+ * elements offset .. offset+n-1 of the SplitMix64 stream of `seed`
+ * (kernels.py:253-290) through the weight transform (u / 2^24) * 0.2 - 0.1
+ * in float64 (kernels.py:292-309), cast to dtype; RNNB_DT_U64 writes the raw
+ * 64-bit outputs.  generate_weights / generate_sequence (model_io.py:157-188)
+ * are this stream in canonical field order. */
+rnnb_status rnnb_splitmix_uniform(uint64_t seed, uint64_t offset, int64_t n, void* out, int dtype,
+                                  void* stream);
 
 /* ---- LSTM partial precompute ----
  * lstm_run_precomputed(w, X, block_size)  blocked.py:271-305, one layer:

@@ -14,7 +14,7 @@ LIB_PATH = os.environ.get("RNNB_LIB", os.path.join(HERE, "librnnb.so"))  # overr
 OK, EINVAL, ECUDA, ENOMEM, EUNSUPPORTED, EFORMAT = 0, 1, 2, 3, 4, 5
 SRU, QRNN = 1, 2
 MODES = {"f32": 0, "f64": 1, "bf16": 2, "tf32": 3, "f32x3": 4}
-DT_F32, DT_F64 = 0, 1
+DT_F32, DT_F64, DT_U64 = 0, 1, 2
 
 # every symbol include/rnnb.h declares (checked by tests/test_abi.py)
 SYMBOLS = (
@@ -26,7 +26,7 @@ SYMBOLS = (
     "rnnb_stack_load_rnnw", "rnnb_lstm_load_rnnw", "rnnb_rnnx_info", "rnnb_rnnx_load",
     "rnnb_forward_ex", "rnnb_dev_alloc", "rnnb_dev_free", "rnnb_ipc_handle", "rnnb_ipc_open",
     "rnnb_ipc_close", "rnnb_peer_access", "rnnb_flag_signal", "rnnb_flag_wait",
-    "rnnb_gemm", "rnnb_activation",
+    "rnnb_gemm", "rnnb_activation", "rnnb_splitmix_uniform",
 )
 MAX_PEERS = 7
 IPC_HANDLE_BYTES = 64
@@ -88,6 +88,7 @@ def load():
         "rnnb_flag_wait": ([ci, vp, ctypes.c_uint32, vp], ci),
         "rnnb_gemm": ([ci, vp, i64, vp, i64, vp, i64, i64, i64, i64, ci, vp], ci),
         "rnnb_activation": ([ci, vp, vp, i64, ci, vp], ci),
+        "rnnb_splitmix_uniform": ([ctypes.c_uint64, ctypes.c_uint64, i64, vp, ci, vp], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

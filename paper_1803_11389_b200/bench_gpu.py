@@ -231,42 +231,42 @@ def _blocks(text):
 
 
 def _model(args):
+    """cli.py:100-130: weights from generate_weights(cfg, seed) (the
+    reference's SplitMix64 stream, generated on the GPU: byte-identical to
+    rnnblock's for the same seed) or a file; the input from
+    generate_sequence(seq_len, d_in, seed + 1) or a file."""
     if args.weights:
         ws = model_io.load_weights(args.weights)
-        X = model_io.load_sequence(args.input) if args.input else None
         cfg = model_io.config_of(ws)
     else:
         kind = CellKind.parse(args.cell)
         d = args.width or PRESET_WIDTH[kind][args.preset]
         cfg = RnnConfig(kind, d, d, n_layers=args.layers, precision=args.precision)
-        ws = _generate(cfg, args.seed)
-        X = None
-    if X is None:
-        rng = np.random.default_rng(args.seed + 1)
-        X = rng.standard_normal((args.seq_len, cfg.d_in)).astype(np.float32 if cfg.precision == "f32" else np.float64)
+        ws = model_io.generate_weights(cfg, args.seed)
+    if args.input:
+        X = model_io.load_sequence(args.input)
+    else:
+        X = model_io.generate_sequence(args.seq_len, cfg.d_in, args.seed + 1, cfg.precision)
     return cfg, ws, X
-
-
-def _generate(cfg, seed):
-    """U(+-1/sqrt(fan_in)) weights from numpy PCG64 (synthetic; the
-    reference's SplitMix64 stream is restated in oracle/ for tests only)."""
-    rng = np.random.default_rng(seed)
-    dt = cfg.dtype
-    cls = {CellKind.LSTM: LstmWeights, CellKind.SRU: SruWeights, CellKind.QRNN: QrnnWeights}[cfg.kind]
-    layers = []
-    for li in range(cfg.n_layers):
-        d_in, d_h = (cfg.d_in if li == 0 else cfg.d_h), cfg.d_h
-        mats = []
-        for shape in model_io.layer_spec(cfg.kind, d_in, d_h):
-            s = 1.0 / np.sqrt(shape[-1] * (2 if cfg.kind is CellKind.QRNN else 1)) if len(shape) == 2 else 0.0
-            mats.append(rng.uniform(-s, s, shape).astype(dt) if len(shape) == 2 else np.zeros(shape, dt))
-        layers.append(cls(*mats))
-    return WeightSet(cfg.kind, cfg.precision, layers)
 
 
 def main(argv=None):
     p = argparse.ArgumentParser(prog="paper_1803_11389_b200.bench_gpu")
     sub = p.add_subparsers(dest="cmd", required=True)
+    g = sub.add_parser("gen-weights", help="generate a weight file (cli.py:144-148)")
+    g.add_argument("--cell", choices=["lstm", "sru", "qrnn"], default="qrnn")
+    g.add_argument("--preset", choices=["small", "large"], default="small")
+    g.add_argument("--width", type=int)
+    g.add_argument("--layers", type=int, default=1)
+    g.add_argument("--precision", choices=["f32", "f64"], default="f32")
+    g.add_argument("--seed", type=int, default=42)
+    g.add_argument("--out", required=True)
+    g = sub.add_parser("gen-seq", help="generate an input-sequence file (cli.py:151-155)")
+    g.add_argument("--seq-len", type=int, default=1024)
+    g.add_argument("--width", type=int, required=True)
+    g.add_argument("--precision", choices=["f32", "f64"], default="f32")
+    g.add_argument("--seed", type=int, default=42)
+    g.add_argument("--out", required=True)
     for name in ("bench", "verify", "traffic"):
         s = sub.add_parser(name)
         s.add_argument("--cell", choices=["lstm", "sru", "qrnn"], default="qrnn")
@@ -283,7 +283,30 @@ def main(argv=None):
         if name == "bench":
             s.add_argument("--repeats", type=int, default=5)
             s.add_argument("--skip-verify", action="store_true")
+            # cli.py's CPU worker count; accepted for drop-in use, the GPU
+            # kernels' results never depend on a thread count
+            s.add_argument("--threads", type=int, default=1)
     args = p.parse_args(argv)
+    if args.cmd == "gen-weights":
+        kind = CellKind.parse(args.cell)
+        d = args.width or PRESET_WIDTH[kind][args.preset]
+        try:
+            cfg = RnnConfig(kind, d, d, n_layers=args.layers, precision=args.precision)
+        except ValueError as e:
+            print(f"error: {e}", file=sys.stderr)
+            return 2
+        model_io.save_weights(model_io.generate_weights(cfg, args.seed), args.out)
+        print(f"wrote {cfg.precision} {cfg.kind.value} weights (d={cfg.d_h}) to {args.out}")
+        return 0
+    if args.cmd == "gen-seq":
+        try:
+            X = model_io.generate_sequence(args.seq_len, args.width, args.seed, args.precision)
+        except ValueError as e:
+            print(f"error: {e}", file=sys.stderr)
+            return 2
+        model_io.save_sequence(X, args.out)
+        print(f"wrote {args.seq_len}x{args.width} {args.precision} sequence to {args.out}")
+        return 0
     try:
         cfg, ws, X = _model(args)
     except model_io.FileFormatError as e:

@@ -92,9 +92,51 @@ cudaError_t gemm_t(bool strict, const void* A, int64_t lda, const void* B, int64
   return cudaGetLastError();
 }
 
+// SplitMix64 (kernels.py:253-309): output j (0-based) of the stream seeded
+// with `seed` is mix(seed + (j + 1) * gamma); the weight transform maps its
+// top 24 bits u to (u / 2^24) * 0.2 - 0.1 in float64, then casts.  Every
+// element is independent, so the stream is generated in parallel.
+__device__ __forceinline__ uint64_t sm64_at(uint64_t seed, uint64_t j) {
+  uint64_t z = seed + (j + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+template <typename T>
+__global__ void splitmix_uniform_kernel(uint64_t seed, uint64_t offset, int64_t n, T* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = sm64_at(seed, offset + (uint64_t)i) >> 40;
+    const double v = __dadd_rn(__dmul_rn(__ddiv_rn((double)u, 16777216.0), 0.2), -0.1);
+    out[i] = (T)v;
+  }
+}
+
+__global__ void splitmix_raw_kernel(uint64_t seed, uint64_t offset, int64_t n, uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = sm64_at(seed, offset + (uint64_t)i);
+}
+
 }  // namespace
 
 extern "C" {
+
+rnnb_status rnnb_splitmix_uniform(uint64_t seed, uint64_t offset, int64_t n, void* out, int dtype, void* stream) {
+  if (n < 0) return set_error(RNNB_EINVAL, "negative length");
+  if (n == 0) return RNNB_OK;
+  if (!out) return set_error(RNNB_EINVAL, "null output");
+  const int bs = 256;
+  const int grid = (int)((n + bs - 1) / bs < 148 * 16 ? (n + bs - 1) / bs : 148 * 16);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == RNNB_DT_F32) splitmix_uniform_kernel<float><<<grid, bs, 0, s>>>(seed, offset, n, static_cast<float*>(out));
+  else if (dtype == RNNB_DT_F64) splitmix_uniform_kernel<double><<<grid, bs, 0, s>>>(seed, offset, n, static_cast<double*>(out));
+  else if (dtype == RNNB_DT_U64) splitmix_raw_kernel<<<grid, bs, 0, s>>>(seed, offset, n, static_cast<uint64_t*>(out));
+  else return set_error(RNNB_EINVAL, "dtype must be f32, f64 or u64 (raw stream)");
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(RNNB_ECUDA, std::string("splitmix launch: ") + cudaGetErrorString(e));
+  return RNNB_OK;
+}
+
 
 rnnb_status rnnb_gemm(int strict, const void* A, int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc,
                       int64_t m, int64_t n, int64_t k, int dtype, void* stream) {

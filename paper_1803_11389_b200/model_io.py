@@ -229,3 +229,58 @@ def load_sequence_device(path, dtype=None, device=None, stream=None):
 def config_of(ws: WeightSet) -> RnnConfig:
     first = ws.layers[0]
     return RnnConfig(ws.kind, first.d_in, first.d_h, n_layers=len(ws.layers), precision=ws.precision)
+
+
+# ---------------------------------------------------------------------------
+# deterministic generation (model_io.py:147-188) on the device
+
+
+def count_params(cfg: RnnConfig) -> int:
+    """model_io.py:147-152."""
+    total = 0
+    for layer in range(cfg.n_layers):
+        d_in, d_h = cfg.layer_dims(layer)
+        total += sum(int(np.prod(s)) for s in layer_spec(cfg.kind, d_in, d_h))
+    return total
+
+
+def _splitmix_uniform(seed, n, dtype):
+    """Elements 0..n-1 of SplitMix64(seed) through the weight transform, cast
+    to dtype -- generated on the GPU (rnnb_splitmix_uniform), copied back."""
+    import torch
+    if not torch.cuda.is_available():
+        raise _lib.RnnbError("CUDA is not available: generation runs on the GPU (no CPU fallback)")
+    lib = _lib.load()
+    tdt = torch.float32 if np.dtype(dtype) == np.float32 else torch.float64
+    out = torch.empty(max(int(n), 1), dtype=tdt, device="cuda")
+    _lib.check(lib.rnnb_splitmix_uniform(ctypes.c_uint64(int(seed) & 0xFFFFFFFFFFFFFFFF), ctypes.c_uint64(0),
+                                         int(n), ctypes.c_void_p(out.data_ptr()),
+                                         _lib.DT_F32 if tdt == torch.float32 else _lib.DT_F64,
+                                         ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out[:n].cpu().numpy()
+
+
+def generate_weights(cfg: RnnConfig, seed: int) -> WeightSet:
+    """Every parameter from one SplitMix64 stream in canonical order, the
+    transform in float64 then cast (model_io.py:155-177): byte-identical to
+    the reference's weights for the same (cfg, seed)."""
+    values = _splitmix_uniform(seed, count_params(cfg), cfg.dtype)
+    layers, pos = [], 0
+    for layer in range(cfg.n_layers):
+        d_in, d_h = cfg.layer_dims(layer)
+        arrays = []
+        for shape in layer_spec(cfg.kind, d_in, d_h):
+            n = int(np.prod(shape))
+            arrays.append(np.ascontiguousarray(values[pos:pos + n].reshape(shape)))
+            pos += n
+        layers.append(_LAYER_CLASS[cfg.kind](*arrays))
+    return WeightSet(kind=cfg.kind, precision=cfg.precision, layers=layers)
+
+
+def generate_sequence(seq_len: int, width: int, seed: int, precision: str = "f32") -> np.ndarray:
+    """Input matrix [seq_len x width] from SplitMix64(seed) (model_io.py:180-188)."""
+    if seq_len < 1 or width < 1:
+        raise ValueError("seq_len and width must be >= 1")
+    if precision not in PRECISIONS:
+        raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
+    return _splitmix_uniform(seed, seq_len * width, PRECISIONS[precision]).reshape(seq_len, width)
