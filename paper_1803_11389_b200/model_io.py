@@ -284,3 +284,21 @@ def generate_sequence(seq_len: int, width: int, seed: int, precision: str = "f32
     if precision not in PRECISIONS:
         raise ValueError(f"precision must be one of {sorted(PRECISIONS)}")
     return _splitmix_uniform(seed, seq_len * width, PRECISIONS[precision]).reshape(seq_len, width)
+
+
+PRESETS = {
+    "lstm-small": (CellKind.LSTM, 350),
+    "lstm-large": (CellKind.LSTM, 700),
+    "sru-small": (CellKind.SRU, 512),
+    "sru-large": (CellKind.SRU, 1024),
+    "qrnn-small": (CellKind.QRNN, 512),
+    "qrnn-large": (CellKind.QRNN, 1024),
+}
+
+
+def preset_config(name: str, precision: str = "f32", n_layers: int = 1) -> RnnConfig:
+    """The paper's model sizes (model_io.py:116-130)."""
+    if name not in PRESETS:
+        raise ValueError(f"unknown preset {name!r}; expected one of {sorted(PRESETS)}")
+    kind, width = PRESETS[name]
+    return RnnConfig(kind=kind, d_in=width, d_h=width, n_layers=n_layers, precision=precision)

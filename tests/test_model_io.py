@@ -115,3 +115,14 @@ def test_sequence_file_errors(M, tmp_path):
     _both(M, p, M.ShapeConsistencyError, weights=False)
     p.write_bytes(good[:12] + struct.pack("<I", 0) + good[16:])
     _both(M, p, M.ShapeConsistencyError, weights=False)
+
+
+def test_presets_and_param_counts():
+    from paper_1803_11389_b200 import model_io as M
+    from paper_1803_11389_b200.cells import CellKind
+    cfg = M.preset_config("qrnn-large")
+    assert (cfg.kind, cfg.d_in, cfg.d_h) == (CellKind.QRNN, 1024, 1024)
+    assert M.count_params(cfg) == 6 * 1024 * 1024  # BASELINE cfg2's 6,291,456 parameters
+    assert M.count_params(M.preset_config("sru-small")) == 3 * 512 * 512 + 2 * 512
+    with pytest.raises(ValueError, match="unknown preset"):
+        M.preset_config("gru-small")
