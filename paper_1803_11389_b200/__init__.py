@@ -38,6 +38,21 @@ from .cells import (
     zero_state,
 )
 from .device import DeviceLstm, DeviceStack
+from .bench_gpu import BenchRecord, BenchResult, SpeedupRow, bench, emit_csv, speedup, summarize, verify
+from .kernels import Rng64, gemm, gemv, sigmoid, tanh_act, uniform_weight
+from .model_io import (
+    PRESETS,
+    count_params,
+    generate_sequence,
+    generate_weights,
+    load_sequence,
+    load_weights,
+    preset_config,
+    save_sequence,
+    save_weights,
+)
+from .stepwise import lstm_step, qrnn_step, run_stepwise, sru_step
+from .traffic import TrafficReport, estimate_traffic, validate_against_trace, weight_bytes
 
 __version__ = "0.1.0"
 
@@ -47,4 +62,11 @@ __all__ = [
     "precompute_gates_qrnn", "precompute_gates_sru", "recurrence_sweep", "run_blocked",
     "PRECISIONS", "CellKind", "CellState", "QrnnWeights", "RnnConfig", "SruWeights",
     "WeightSet", "zero_state", "DeviceStack", "LstmWeights", "DeviceLstm",
+    # the rest of rnnblock's top-level names (rnnblock/__init__.py)
+    "BenchRecord", "BenchResult", "SpeedupRow", "bench", "emit_csv", "speedup", "summarize", "verify",
+    "Rng64", "gemm", "gemv", "sigmoid", "tanh_act", "uniform_weight",
+    "PRESETS", "count_params", "generate_sequence", "generate_weights", "load_sequence", "load_weights",
+    "preset_config", "save_sequence", "save_weights",
+    "lstm_step", "qrnn_step", "run_stepwise", "sru_step",
+    "TrafficReport", "estimate_traffic", "validate_against_trace", "weight_bytes",
 ]

@@ -149,3 +149,34 @@ def get_compute_threads() -> int:
     if _threads is None:
         return set_compute_threads(1 << 30)
     return _threads
+
+
+# ---------------------------------------------------------------------------
+# the reference's PRNG utilities (kernels.py:253-309): host-side scalar
+# helpers for callers that draw values one at a time; bulk streams are
+# generated on the GPU (model_io.generate_weights / generate_sequence)
+
+_MASK64 = (1 << 64) - 1
+
+
+class Rng64:
+    """SplitMix64 stream (kernels.py:253-269); from seed 0 the first output
+    is 0xE220A8397B1DCDAF."""
+
+    def __init__(self, seed: int):
+        self.state = seed & _MASK64
+
+    def next(self) -> int:
+        self.state = (self.state + 0x9E3779B97F4A7C15) & _MASK64
+        z = self.state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK64
+        return z ^ (z >> 31)
+
+
+def uniform_weight(raw: int) -> float:
+    """Top 24 bits of a raw draw to [-0.1, 0.1): (u / 2^24) * 0.2 - 0.1 in
+    float64, in this operation order (kernels.py:292-299)."""
+    u = (int(raw) & _MASK64) >> 40
+    return (u / 16777216.0) * 0.2 - 0.1
+

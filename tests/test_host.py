@@ -91,3 +91,22 @@ def test_product_path_has_no_cpu_fallback():
     cfg = P.RnnConfig(P.CellKind.SRU, 4, 4)
     with pytest.raises(RuntimeError):
         P.run_blocked(cfg, P.WeightSet(P.CellKind.SRU, "f32", [w]), np.zeros((3, 4), np.float32), 2)
+
+
+def test_top_level_names_match_the_reference_package():
+    """Every name rnnblock/__init__.py exports exists at our package's top
+    level (drop-in `import paper_1803_11389_b200 as rnnblock`); the list is
+    the reference's own export list, restated."""
+    import paper_1803_11389_b200 as P
+    names = ["BenchRecord", "BenchResult", "SpeedupRow", "bench", "emit_csv", "speedup", "summarize", "verify",
+             "BlockPlan", "GateBlock", "KernelTrace", "finalize_outputs", "lstm_run_precomputed", "plan_blocks",
+             "precompute_gates_qrnn", "precompute_gates_sru", "recurrence_sweep", "run_blocked",
+             "CellKind", "CellState", "LstmWeights", "QrnnWeights", "SruWeights", "lstm_step", "qrnn_step",
+             "run_stepwise", "sru_step", "zero_state", "Rng64", "gemm", "gemv", "sigmoid", "tanh_act",
+             "uniform_weight", "PRESETS", "RnnConfig", "WeightSet", "count_params", "generate_sequence",
+             "generate_weights", "load_sequence", "load_weights", "preset_config", "save_sequence",
+             "save_weights", "TrafficReport", "estimate_traffic", "validate_against_trace", "weight_bytes"]
+    missing = [n for n in names if not hasattr(P, n)]
+    assert not missing, missing
+    assert P.Rng64(0).next() == 0xE220A8397B1DCDAF
+    assert P.uniform_weight(0) == -0.1
