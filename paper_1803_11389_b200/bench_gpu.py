@@ -124,11 +124,16 @@ class BenchResult:
     threads: int = 0
 
 
-def bench(cfg, weights, X, t_list, repeats: int = 5, warmup: int = 1) -> BenchResult:
-    """CUDA-event timed forwards of the whole sequence per block size."""
+def bench(cfg, weights, X, t_list, repeats: int = 5, threads: int = 1, warmup: int = 1) -> BenchResult:
+    """CUDA-event timed forwards of the whole sequence per block size
+    (bench.py:124-153's signature; `threads`, the reference's CPU worker
+    count, is validated and otherwise unused: the GPU result and timing do
+    not depend on it, and records carry the multiprocessor count)."""
     import torch
     if repeats < 1:
         raise ValueError("repeats must be >= 1")
+    if threads < 1:
+        raise ValueError("threads must be >= 1")
     sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
     result = BenchResult(threads=sms)
     impl = "gpu-lstm-precomputed" if cfg.kind is CellKind.LSTM else "gpu-blocked"
