@@ -15,6 +15,21 @@ NAMES = {"gpu__time_duration.sum": ("us", 1e-3), "dram__bytes_read.sum": ("dram_
          "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum": ("smem_wavefronts_M", 1e-6)}
 
 
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _peak(path, key, default):
+    try:
+        with open(os.path.join(REPO, path)) as f:
+            return json.load(f)[key]
+    except (OSError, KeyError, ValueError):
+        return default
+
+
+HBM_GBS = _peak("MEASURED_PEAKS.json", "hbm_gbs", 6543.7)
+L2_GBS = _peak("profiles/l2_peak.json", "l2_read_gbs", 11781.8)
+
+
 def main(d):
     rows = []
     for f in sorted(os.listdir(d)):
@@ -29,10 +44,20 @@ def main(d):
                 name, scale = NAMES[key]
                 rec[name] = round(float(r["Metric Value"].replace(",", "")) * scale, 2)
             rec["kernel"] = r["Kernel Name"].split("<")[0].replace("void rnnb::", "").replace("void ", "")
+        # achieved bandwidths against the measured peaks (per launch)
+        if rec.get("us"):
+            sec = rec["us"] * 1e-6
+            rec["dram_gbs"] = round(rec.get("dram_MB", 0) * 1e6 / sec / 1e9, 1)
+            rec["l2_gbs"] = round(rec.get("l2_MB", 0) * 1e6 / sec / 1e9, 1)
+            rec["dram_frac"] = round(rec["dram_gbs"] / HBM_GBS, 4)
+            rec["l2_frac"] = round(rec["l2_gbs"] / L2_GBS, 4)
         rows.append(rec)
     rows.sort(key=lambda r: (r["mode"], r["T_b"]))
     print(json.dumps({"what": "ncu --metrics (one launch, cold caches) of the blocked-layer kernel on cfg2 "
-                              "(QRNN 1024, L=2048) per mode and T_b; tools/ncu_sweep.sh", "rows": rows}, indent=1))
+                              "(QRNN 1024, L=2048) per mode and T_b; tools/ncu_sweep.sh.  dram/l2 GB/s = "
+                              "measured bytes / kernel time, fractions against MEASURED_PEAKS.json hbm_gbs "
+                              f"({HBM_GBS}) and profiles/l2_peak.json ({L2_GBS}); tensor_pct / fma_pct = "
+                              "pipe utilisation", "rows": rows}, indent=1))
 
 
 if __name__ == "__main__":
