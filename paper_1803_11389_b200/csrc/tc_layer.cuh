@@ -171,6 +171,17 @@ __device__ __forceinline__ float ld_cg(const float* p) {
   asm volatile("ld.global.cg.f32 %0, [%1];\n" : "=f"(v) : "l"(p) : "memory");
   return v;
 }
+// Branch-free tanh for the epilogue: 1 - 2 / (e^{2|x|} + 1) with the sign
+// restored, on MUFU ex2 / rcp.  Absolute error ~2e-7 (|x| clamped at 15, where
+// tanh rounds to 1 in fp32), inside the fp32 bound the tensor-core modes are
+// held to; the library tanhf branches on |x| and, with one epilogue warp per
+// scheduler, its dependent MUFU chain made the epilogue latency-bound.
+__device__ __forceinline__ float tc_tanh(float x) {
+  const float e = __expf(2.f * fminf(fabsf(x), 15.f));
+  return copysignf(1.f - __fdividef(2.f, e + 1.f), x);
+}
+__device__ __forceinline__ float tc_sigmoid(float z) { return 0.5f * (1.f + tc_tanh(0.5f * z)); }
+
 // named barrier 2 over the four epilogue warps
 __device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
 
@@ -185,10 +196,14 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
   const size_t sidx = (size_t)b * a.Hpad + unit;
   a.aggA[sidx] = Ablk;
   a.aggB[sidx] = Bblk;
-  __threadfence();
+  // the barrier orders the 128 threads' stores before thread 0's gpu-scope
+  // fence + release (cumulativity), one fence per item instead of 128
   tc_epi_sync();
   const int tag = 4 * a.epoch;
-  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 1);
+  if (et == 0) {
+    __threadfence();
+    st_release(&a.status[(size_t)b * a.nU + u], tag + 1);
+  }
   const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
   // lanes of the first epilogue warp wait for the statuses in parallel
   if (et < 32) {
@@ -209,9 +224,11 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
                                 : (a.c_in != nullptr && unit < a.H ? a.c_in[unit] : 0.f);
   const float cin = Aacc * anchor + Bacc;
   a.incl[sidx] = Ablk * cin + Bblk;
-  __threadfence();
   tc_epi_sync();
-  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
+  if (et == 0) {
+    __threadfence();
+    st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
+  }
   return cin;
 }
 
@@ -406,12 +423,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           if (CELL == SRU) {
-            rf[j] = sigmoid_ref<float>(rf[j] + bf);
-            ro[j] = sigmoid_ref<float>(ro[j] + br);
+            rf[j] = tc_sigmoid(rf[j] + bf);
+            ro[j] = tc_sigmoid(ro[j] + br);
           } else {
-            rz[j] = tanh_full(rz[j]);
-            rf[j] = sigmoid_ref<float>(rf[j]);
-            ro[j] = sigmoid_ref<float>(ro[j]);
+            rz[j] = tc_tanh(rz[j]);
+            rf[j] = tc_sigmoid(rf[j]);
+            ro[j] = tc_sigmoid(ro[j]);
           }
           if (j < l) {
             Bblk = rf[j] * Bblk + (1.f - rf[j]) * rz[j];
@@ -424,7 +441,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int j = 0; j < N; ++j) {
           if (j < l && unit < a.H) {
             c = rf[j] * c + (1.f - rf[j]) * rz[j];
-            float h = ro[j] * tanh_full(c);
+            float h = ro[j] * tc_tanh(c);
             if (CELL == SRU) h = h + (1.f - ro[j]) * a.Xhw[(t0 + j) * a.ldhw + unit];
             store_h(a, (t0 + j) * a.ldh + unit, h);
           }
@@ -445,12 +462,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           if (CELL == SRU) {
-            pf[j] = sigmoid_ref<float>(pf[j] + bf);
-            po[j] = sigmoid_ref<float>(po[j] + br);
+            pf[j] = tc_sigmoid(pf[j] + bf);
+            po[j] = tc_sigmoid(po[j] + br);
           } else {
-            pz[j] = tanh_full(pz[j]);
-            pf[j] = sigmoid_ref<float>(pf[j]);
-            po[j] = sigmoid_ref<float>(po[j]);
+            pz[j] = tc_tanh(pz[j]);
+            pf[j] = tc_sigmoid(pf[j]);
+            po[j] = tc_sigmoid(po[j]);
           }
           if (c0 + j < l) {
             Bblk = pf[j] * Bblk + (1.f - pf[j]) * pz[j];
@@ -464,7 +481,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tmem_st_wait();
       const float cin = tc_lookback(a, b, u, unit, et, Ablk, Bblk);
       // (C) sequential recurrence from c_in and the output mix
+      // row pointers advanced by a stride per step (no 64-bit index
+      // arithmetic per store); the uniform peer / operand-copy tests hoisted
       float c = cin;
+      const bool live = unit < a.H;
+      const int64_t ldh = a.ldh, ldhw = a.ldhw, ldop = a.ldop;
+      const int npeer = a.npeer;
+      float* hp = a.Hout + t0 * ldh + unit;
+      const float* xp = CELL == SRU ? a.Xhw + t0 * ldhw + unit : nullptr;
+      unsigned char* op = a.Hop ? static_cast<unsigned char*>(a.Hop) +
+                                      (t0 * ldop + unit) * (MODE == TC_BF16 ? 2 : 4)
+                                : nullptr;
       for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
         float z[16], f[16], o[16];
         tmem_ld16(tb + 0 * N + c0, z);
@@ -473,16 +500,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int col = c0 + j;
-          if (col < l && unit < a.H) {
+          if (col < l && live) {
             c = f[j] * c + (1.f - f[j]) * z[j];
-            float h = o[j] * tanh_full(c);
-            if (CELL == SRU) h = h + (1.f - o[j]) * a.Xhw[(t0 + col) * a.ldhw + unit];
-            store_h(a, (t0 + col) * a.ldh + unit, h);
-            if (a.Hop) {
+            float h = o[j] * tc_tanh(c);
+            if (CELL == SRU) h = h + (1.f - o[j]) * xp[(int64_t)col * ldhw];
+            hp[(int64_t)col * ldh] = h;
+            if (npeer > 0) {
+              const int64_t i = (t0 + col) * ldh + unit;
+#pragma unroll
+              for (int p = 0; p < kMaxPeers; ++p)
+                if (p < npeer) a.Hpeer[p][i] = h;
+            }
+            if (op != nullptr) {
               if (MODE == TC_BF16)
-                reinterpret_cast<__nv_bfloat16*>(a.Hop)[(t0 + col) * a.ldop + unit] = __float2bfloat16_rn(h);
+                reinterpret_cast<__nv_bfloat16*>(op)[(int64_t)col * ldop] = __float2bfloat16_rn(h);
               else
-                reinterpret_cast<float*>(a.Hop)[(t0 + col) * a.ldop + unit] = round_x(h, XR_TF32);
+                reinterpret_cast<float*>(op)[(int64_t)col * ldop] = round_x(h, XR_TF32);
             }
           }
         }
