@@ -106,8 +106,20 @@ static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUten
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k<<<grid, kTcThreads, C::SMEM, s>>>(a, tw, tx);
-  return cudaGetLastError();
+  // programmatic dependent launch: the CTAs set up (barriers, TMEM, tensor-map
+  // prefetch) while the preceding kernel -- usually the operand conversion --
+  // drains, then wait on griddepcontrol before touching global memory
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute attrs[1];
+  attrs[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attrs[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attrs;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a, tw, tx);
 }
 
 int tc_max_n(int mode) { return mode == TC_3XTF32 ? 32 : 128; }
