@@ -180,7 +180,10 @@ rnnb_status rnnb_lstm_forward(rnnb_lstm_t h, const void* X, int64_t ldx, int64_t
 rnnb_status rnnb_lstm_forward_host(rnnb_lstm_t h, const void* X, int64_t L, int64_t block_size, void* H,
                                    void* c_state, void* h_state, void* stream);
 /* what: 0 weight bytes, 1 launches of the last forward, 2 units per CTA,
- * 3 = 1 if the CTA's U rows were shared-memory resident, 4 grid size. */
+ * 3 = 1 if the CTA's U rows were shared-memory resident, 4 grid size,
+ * 5 CTAs of the one-cluster recurrence used by the last forward (0: the
+ * grid kernel; fp32 layers whose U fits one 16-CTA cluster, d_h <= ~470;
+ * RNNB_LSTM_CLUSTER=0 disables it). */
 rnnb_status rnnb_lstm_query(rnnb_lstm_t h, int what, int64_t* value);
 
 /* ---- RNNW / RNNX files -> device ----

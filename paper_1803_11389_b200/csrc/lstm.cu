@@ -301,6 +301,127 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_rec_kernel(LstmRecArgs a)
   }
 }
 
+// Small layers (fp32, the whole of U fits in one 16-CTA cluster's shared
+// memory -- d_h up to ~470): the recurrence runs inside ONE thread-block
+// cluster.  Every CTA keeps h_{t-1} in a double-buffered shared vector that
+// the owners of each unit write directly (st.shared::cluster into every
+// CTA of the cluster), and one cluster barrier (arrive.release /
+// wait.acquire) per step replaces the global flags and the L2 gather: no
+// global round trip on the recurrence chain.  Unit ownership differs from the
+// grid kernel (ceil(H/CS) units per CTA), the row layout of U and Gx does not.
+constexpr int kClusterCTAs = 16;  // non-portable cluster size (B200 allows 16)
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_f32(const float* local, uint32_t rank, float v) {
+  uint32_t la = (uint32_t)__cvta_generic_to_shared(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;\n" ::"r"(ra), "f"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int NW = kRecThreads / 32;
+  uint32_t rank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(rank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(csize));
+  const int Uc = a.U, Kh = a.Kh;
+  const int u0 = (int)rank * Uc;
+  const int nu = a.H - u0 < Uc ? (a.H - u0 > 0 ? a.H - u0 : 0) : Uc;  // units this CTA owns
+  const int R = 4 * nu;
+  float* hs = reinterpret_cast<float*>(smem_raw);  // [2][Kh]: h_{t-1} by step parity
+  float* pre = hs + 2 * Kh;                        // [4 Uc]
+  float* Us = pre + ((4 * Uc + 3) / 4) * 4;        // [4 Uc][Kh]
+  const float* Ug = static_cast<const float*>(a.Ur) + (size_t)u0 * 4 * Kh;
+  for (int i = tid; i < R * Kh; i += kRecThreads) Us[i] = Ug[i];
+  for (int i = tid; i < 2 * Kh; i += kRecThreads) hs[i] = 0.f;  // padding columns stay 0
+  const float* Gx = static_cast<const float*>(a.Gx);
+  float* Hout = static_cast<float*>(a.Hout);
+  const bool own = tid < nu;
+  float c = 0.f, hcur = 0.f;
+  if (own) {
+    if (a.c_io) c = static_cast<const float*>(a.c_io)[u0 + tid];
+    if (a.h_io) hcur = static_cast<const float*>(a.h_io)[u0 + tid];
+  }
+  cluster_sync_all();  // every CTA zeroed its vector before anyone writes into it
+  if (own)
+    for (uint32_t q = 0; q < csize; ++q) st_cluster_f32(&hs[u0 + tid], q, hcur);
+  float gx[4] = {0.f, 0.f, 0.f, 0.f}, gn[4] = {0.f, 0.f, 0.f, 0.f};
+  auto load_gx = [&](int64_t t, float (&dst)[4]) {
+    if (own && t < a.L) {
+      const float* gp = Gx + (size_t)t * 4 * a.Hp + (size_t)(u0 + tid) * 4;
+#pragma unroll
+      for (int g = 0; g < 4; ++g) dst[g] = gp[g];
+    }
+  };
+  load_gx(0, gn);
+  cluster_sync_all();  // h_{-1} complete in every CTA
+  for (int64_t t = 0; t < a.L; ++t) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) gx[g] = gn[g];
+    load_gx(t + 1, gn);
+    const float* hsrc = hs + (size_t)(t & 1) * Kh;
+    // rows warp, warp + NW, ... three at a time (independent chains share
+    // each h load); per row the same per-lane ascending-k float4 order and
+    // butterfly as dot_row, so the products equal the grid kernel's bitwise
+    for (int r0 = warp; r0 < R; r0 += 3 * NW) {
+      float4 acc[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int k = 4 * lane; k < Kh; k += 128) {
+        const float4 x = *reinterpret_cast<const float4*>(hsrc + k);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int r = r0 + q * NW;
+          if (r < R) {
+            const float4 u = *reinterpret_cast<const float4*>(Us + (size_t)r * Kh + k);
+            acc[q].x = fmaf(u.x, x.x, acc[q].x);
+            acc[q].y = fmaf(u.y, x.y, acc[q].y);
+            acc[q].z = fmaf(u.z, x.z, acc[q].z);
+            acc[q].w = fmaf(u.w, x.w, acc[q].w);
+          }
+        }
+      }
+      float v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) v[q] = (acc[q].x + acc[q].y) + (acc[q].z + acc[q].w);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+          if (r0 + q * NW < R) pre[r0 + q * NW] = v[q];
+    }
+    __syncthreads();
+    if (own) {
+      const int r = tid * 4;
+      const float f = sigmoid_ref<float>(gx[0] + pre[r + 0]);
+      const float i = sigmoid_ref<float>(gx[1] + pre[r + 1]);
+      const float o = sigmoid_ref<float>(gx[2] + pre[r + 2]);
+      const float cand = tanh_full(gx[3] + pre[r + 3]);
+      c = f * c + i * cand;
+      hcur = o * tanh_full(c);
+      float* dst = hs + (size_t)((t + 1) & 1) * Kh + u0 + tid;
+      for (uint32_t q = 0; q < csize; ++q) st_cluster_f32(dst, q, hcur);
+    }
+    // h_t visible in every CTA, and every CTA done reading h_{t-1}'s buffer
+    // (overwritten at step t+1): one barrier per step.  The global h store
+    // sits between arrive and wait so the release never waits on it.
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    if (own) Hout[t * a.ldh + u0 + tid] = hcur;
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
+  if (own) {
+    if (a.c_io) static_cast<float*>(a.c_io)[u0 + tid] = c;
+    if (a.h_io) static_cast<float*>(a.h_io)[u0 + tid] = hcur;
+  }
+}
+
 }  // namespace rnnb
 
 using namespace rnnb;
@@ -322,6 +443,7 @@ struct rnnb_lstm {
   size_t hx_bytes = 0, hh_bytes = 0;
   int64_t last_launches = 0;
   bool last_resident = false;
+  int last_cluster = 0;  // CTAs of the cluster kernel in the last forward (0: grid kernel)
 };
 
 namespace {
@@ -384,6 +506,42 @@ rnnb_status lstm_forward_t(rnnb_lstm* h, const T* X, int64_t ldx, int64_t L, T* 
   a.Kh = h->Kh;
   a.U = h->U;
   a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
+  // one-cluster recurrence when the whole of U fits in the cluster (fp32)
+  const char* env_cl = getenv("RNNB_LSTM_CLUSTER");
+  if (sizeof(T) == 4 && !(env_cl && atoi(env_cl) == 0)) {
+    const int CS = kClusterCTAs;
+    const int Uc = (int)((h->dh + CS - 1) / CS);
+    const size_t smem_cl = sizeof(float) * (2 * (size_t)h->Kh + (size_t)((4 * Uc + 3) / 4) * 4 + (size_t)4 * Uc * h->Kh);
+    if (smem_cl <= 227 * 1024) {
+      auto kc = lstm_cluster_kernel;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(CS);
+      cfg.blockDim = dim3(kRecThreads);
+      cfg.dynamicSmemBytes = smem_cl;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nclusters = 0;
+      if (cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cl) == cudaSuccess &&
+          cudaFuncSetAttribute(kc, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess &&
+          cudaOccupancyMaxActiveClusters(&nclusters, kc, &cfg) == cudaSuccess && nclusters >= 1) {
+        a.U = Uc;
+        a.resident = 1;
+        LSTM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kc, a));
+        h->last_launches = 2;
+        h->last_resident = true;
+        h->last_cluster = CS;
+        return RNNB_OK;
+      }
+      cudaGetLastError();  // the attribute / occupancy probe failed: grid kernel below
+    }
+  }
+  h->last_cluster = 0;
   const size_t smem_res = rec_smem(h, true);
   a.resident = smem_res <= 227 * 1024 ? 1 : 0;
   const size_t smem = rec_smem(h, a.resident);
@@ -558,6 +716,7 @@ rnnb_status rnnb_lstm_query(rnnb_lstm_t h, int what, int64_t* value) {
     case 2: *value = h->U; return RNNB_OK;
     case 3: *value = h->last_resident ? 1 : 0; return RNNB_OK;
     case 4: *value = h->grid; return RNNB_OK;
+    case 5: *value = h->last_cluster; return RNNB_OK;
     default: return set_error(RNNB_EINVAL, "unknown query");
   }
 }

@@ -130,3 +130,39 @@ def test_lstm_call_counts_and_errors(P, oracle):
         P.lstm_run_precomputed(w, X.astype(np.float64), 4)
     with pytest.raises(ValueError):
         P.lstm_run_precomputed(w, X, 4, kernel="cuda")
+
+
+@pytest.mark.parametrize("din,dh,L", [(350, 350, 257), (64, 64, 100), (7, 5, 33), (512, 470, 65), (96, 17, 40)])
+def test_lstm_cluster_recurrence_vs_oracle(P, oracle, din, dh, L, monkeypatch):
+    """Small fp32 layers run the recurrence inside one 16-CTA cluster (h
+    exchanged through distributed shared memory, one cluster barrier per
+    step); the grid kernel (RNNB_LSTM_CLUSTER=0) must agree with the oracle
+    on the same inputs, and both are deterministic."""
+    import torch
+    w = oracle.generate_layers("lstm", din, dh, 1, 17, np.float32)[0]
+    X = np.random.default_rng(5).standard_normal((L, din)).astype(np.float32)
+    ref = oracle.lstm_blocked(w, X, 8)
+    dev = P.DeviceLstm(w)
+    Xd = torch.from_numpy(X).cuda()
+    H1 = dev.forward(Xd, 8).cpu().numpy()
+    assert dev.query(5) == 16
+    assert_close(H1, ref, np.float32)
+    assert np.array_equal(H1, dev.forward(Xd, 8).cpu().numpy())
+    monkeypatch.setenv("RNNB_LSTM_CLUSTER", "0")
+    H0 = dev.forward(Xd, 8).cpu().numpy()
+    assert dev.query(5) == 0
+    assert_close(H0, ref, np.float32)
+    # same products in the same order on both paths
+    assert np.array_equal(H0, H1)
+    dev.close()
+
+
+def test_lstm_cluster_not_used_when_u_does_not_fit(P, oracle):
+    import torch
+    w = oracle.generate_layers("lstm", 64, 512, 1, 3, np.float32)[0]
+    X = np.random.default_rng(1).standard_normal((20, 64)).astype(np.float32)
+    dev = P.DeviceLstm(w)
+    H = dev.forward(torch.from_numpy(X).cuda(), 4).cpu().numpy()
+    assert dev.query(5) == 0
+    assert_close(H, oracle.lstm_blocked(w, X, 4), np.float32)
+    dev.close()

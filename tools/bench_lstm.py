@@ -51,7 +51,8 @@ def main():
         flops = 2.0 * 4 * d * (d + d) * L
         row = {"d_in": d, "d_h": d, "L": L, "ms": round(ms, 4), "steps_per_s": round(L / ms * 1e3, 1),
                "us_per_step": round(ms * 1e3 / L, 3), "tflops": round(flops / ms / 1e9, 2),
-               "u_resident_smem": bool(dev.query(3)), "units_per_cta": dev.query(2), "grid": dev.query(4)}
+               "u_resident_smem": bool(dev.query(3)), "units_per_cta": dev.query(2), "grid": dev.query(4),
+               "cluster_ctas": dev.query(5)}
         rows.append(row)
         print(row, flush=True)
         dev.close()
