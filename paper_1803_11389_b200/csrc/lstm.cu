@@ -304,10 +304,11 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_rec_kernel(LstmRecArgs a)
 // Small layers (fp32, the whole of U fits in one 16-CTA cluster's shared
 // memory -- d_h up to ~470): the recurrence runs inside ONE thread-block
 // cluster.  Every CTA keeps h_{t-1} in a double-buffered shared vector that
-// the owners of each unit write directly (st.shared::cluster into every
-// CTA of the cluster), and one cluster barrier (arrive.release /
-// wait.acquire) per step replaces the global flags and the L2 gather: no
-// global round trip on the recurrence chain.  Unit ownership differs from the
+// the owners of each unit write directly (st.async into every CTA of the
+// cluster, completing bytes on that CTA's mbarrier for the buffer), so a
+// CTA's wait on its own mbarrier replaces the global flags, the L2 gather
+// and any fence: no global round trip and no memory barrier on the
+// recurrence chain.  Unit ownership differs from the
 // grid kernel (ceil(H/CS) units per CTA), the row layout of U and Gx does not.
 constexpr int kClusterCTAs = 16;  // non-portable cluster size (B200 allows 16)
 
@@ -315,14 +316,29 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void st_cluster_f32(const float* local, uint32_t rank, float v) {
-  uint32_t la = (uint32_t)__cvta_generic_to_shared(local), ra;
+// h value into CTA `rank`'s vector, completing bytes on that CTA's mbarrier
+// for the buffer (st.async: no fence, the receiver's mbarrier wait orders it)
+__device__ __forceinline__ void st_async_f32(const float* local, const uint64_t* mbar, uint32_t rank, float v) {
+  const uint32_t la = (uint32_t)__cvta_generic_to_shared(local), lb = (uint32_t)__cvta_generic_to_shared(mbar);
+  uint32_t ra, rb;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(ra) : "r"(la), "r"(rank));
-  asm volatile("st.shared::cluster.f32 [%0], %1;\n" ::"r"(ra), "f"(v) : "memory");
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(rb) : "r"(lb), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(ra),
+               "r"(__float_as_uint(v)), "r"(rb)
+               : "memory");
+}
+__device__ __forceinline__ void cl_mbar_wait(const uint64_t* mbar, uint32_t parity) {
+  const uint32_t a = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "LW_%=:\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t@!p bra LW_%=;\n\t}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
 }
 
 __global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t hbar[2];  // one mbarrier per h buffer
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int NW = kRecThreads / 32;
   uint32_t rank, csize;
@@ -338,17 +354,23 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArg
   const float* Ug = static_cast<const float*>(a.Ur) + (size_t)u0 * 4 * Kh;
   for (int i = tid; i < R * Kh; i += kRecThreads) Us[i] = Ug[i];
   for (int i = tid; i < 2 * Kh; i += kRecThreads) hs[i] = 0.f;  // padding columns stay 0
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(&hbar[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   const float* Gx = static_cast<const float*>(a.Gx);
   float* Hout = static_cast<float*>(a.Hout);
   const bool own = tid < nu;
+  const uint32_t hbytes = 4u * (uint32_t)a.H;  // every unit's h once per buffer fill
   float c = 0.f, hcur = 0.f;
   if (own) {
     if (a.c_io) c = static_cast<const float*>(a.c_io)[u0 + tid];
     if (a.h_io) hcur = static_cast<const float*>(a.h_io)[u0 + tid];
   }
-  cluster_sync_all();  // every CTA zeroed its vector before anyone writes into it
+  cluster_sync_all();  // barriers initialised and vectors zeroed in every CTA
   if (own)
-    for (uint32_t q = 0; q < csize; ++q) st_cluster_f32(&hs[u0 + tid], q, hcur);
+    for (uint32_t q = 0; q < csize; ++q) st_async_f32(&hs[u0 + tid], &hbar[0], q, hcur);
   float gx[4] = {0.f, 0.f, 0.f, 0.f}, gn[4] = {0.f, 0.f, 0.f, 0.f};
   auto load_gx = [&](int64_t t, float (&dst)[4]) {
     if (own && t < a.L) {
@@ -358,12 +380,22 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArg
     }
   };
   load_gx(0, gn);
-  cluster_sync_all();  // h_{-1} complete in every CTA
+  // Buffer p = t & 1 holds h_{t-1}; its (t >> 1)-th fill.  A CTA sends h_t
+  // into buffer (t+1) & 1 only after it received h_{t-1} from every CTA,
+  // i.e. after every CTA finished reading h_{t-2} from that buffer: the data
+  // flow alone orders the reuse, no cluster barrier per step.
   for (int64_t t = 0; t < a.L; ++t) {
+    const int p = (int)(t & 1);
+    if (tid == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&hbar[p])),
+                   "r"(hbytes)
+                   : "memory");
 #pragma unroll
     for (int g = 0; g < 4; ++g) gx[g] = gn[g];
     load_gx(t + 1, gn);
-    const float* hsrc = hs + (size_t)(t & 1) * Kh;
+    cl_mbar_wait(&hbar[p], (uint32_t)((t >> 1) & 1));
+    const float* hsrc = hs + (size_t)p * Kh;
     // rows warp, warp + NW, ... three at a time (independent chains share
     // each h load); per row the same per-lane ascending-k float4 order and
     // butterfly as dot_row, so the products equal the grid kernel's bitwise
@@ -406,20 +438,20 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArg
       const float cand = tanh_full(gx[3] + pre[r + 3]);
       c = f * c + i * cand;
       hcur = o * tanh_full(c);
-      float* dst = hs + (size_t)((t + 1) & 1) * Kh + u0 + tid;
-      for (uint32_t q = 0; q < csize; ++q) st_cluster_f32(dst, q, hcur);
+      if (t + 1 < a.L) {  // the last h is nobody's input
+        float* dst = hs + (size_t)(p ^ 1) * Kh + u0 + tid;
+        for (uint32_t q = 0; q < csize; ++q) st_async_f32(dst, &hbar[p ^ 1], q, hcur);
+      }
+      Hout[t * a.ldh + u0 + tid] = hcur;
     }
-    // h_t visible in every CTA, and every CTA done reading h_{t-1}'s buffer
-    // (overwritten at step t+1): one barrier per step.  The global h store
-    // sits between arrive and wait so the release never waits on it.
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
-    if (own) Hout[t * a.ldh + u0 + tid] = hcur;
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    // no second barrier: pre[] is rewritten at step t+1 only after this
+    // CTA's own h_t (sent above, after reading pre[]) has arrived
   }
   if (own) {
     if (a.c_io) static_cast<float*>(a.c_io)[u0 + tid] = c;
     if (a.h_io) static_cast<float*>(a.h_io)[u0 + tid] = hcur;
   }
+  cluster_sync_all();  // no CTA leaves while a peer may still address its shared memory
 }
 
 }  // namespace rnnb
