@@ -311,6 +311,10 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_rec_kernel(LstmRecArgs a)
 // recurrence chain.  Unit ownership differs from the
 // grid kernel (ceil(H/CS) units per CTA), the row layout of U and Gx does not.
 constexpr int kClusterCTAs = 16;  // non-portable cluster size (B200 allows 16)
+#ifndef RNNB_LSTM_RB
+#define RNNB_LSTM_RB 6
+#endif
+constexpr int kRB = RNNB_LSTM_RB;  // rows per warp in flight in the cluster GEMV
 
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -396,17 +400,17 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArg
     load_gx(t + 1, gn);
     cl_mbar_wait(&hbar[p], (uint32_t)((t >> 1) & 1));
     const float* hsrc = hs + (size_t)p * Kh;
-    // rows warp, warp + NW, ... three at a time (independent chains share
+    // rows warp, warp + NW, ... kRB at a time (independent chains share
     // each h load); per row the same per-lane ascending-k float4 order and
     // butterfly as dot_row, so the products equal the grid kernel's bitwise
-    for (int r0 = warp; r0 < R; r0 += 3 * NW) {
-      float4 acc[3];
+    for (int r0 = warp; r0 < R; r0 += kRB * NW) {
+      float4 acc[kRB];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < kRB; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int k = 4 * lane; k < Kh; k += 128) {
         const float4 x = *reinterpret_cast<const float4*>(hsrc + k);
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
+        for (int q = 0; q < kRB; ++q) {
           const int r = r0 + q * NW;
           if (r < R) {
             const float4 u = *reinterpret_cast<const float4*>(Us + (size_t)r * Kh + k);
@@ -417,16 +421,16 @@ __global__ void __launch_bounds__(kRecThreads, 1) lstm_cluster_kernel(LstmRecArg
           }
         }
       }
-      float v[3];
+      float v[kRB];
 #pragma unroll
-      for (int q = 0; q < 3; ++q) v[q] = (acc[q].x + acc[q].y) + (acc[q].z + acc[q].w);
+      for (int q = 0; q < kRB; ++q) v[q] = (acc[q].x + acc[q].y) + (acc[q].z + acc[q].w);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+        for (int q = 0; q < kRB; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
       if (lane == 0)
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
+        for (int q = 0; q < kRB; ++q)
           if (r0 + q * NW < R) pre[r0 + q * NW] = v[q];
     }
     __syncthreads();
