@@ -148,6 +148,24 @@ rnnb_status rnnb_gemm(int strict, const void* A, int64_t lda, const void* B, int
                       int64_t ldc, int64_t m, int64_t n, int64_t k, int dtype, void* stream);
 rnnb_status rnnb_activation(int which, const void* x, void* y, int64_t n, int dtype, void* stream);
 
+/* ---- Dense layers (BASELINE cfg3: the acoustic model's 120 -> 1024 input
+ * projection and 1024 -> 2000 logits) ----
+ * Y[L x d_out] = X[L x d_in] W^T (+ b) on DEVICE buffers: the product
+ * kernels.gemm(W, X^T) (kernels.py:203-225) restated for the time-major
+ * layout of the blocked path.  W [d_out x d_in] and the optional bias
+ * [d_out] are HOST arrays of src_dtype, uploaded once.  Modes: RNNB_F32 /
+ * RNNB_F64 (and RNNB_F32X3): FFMA GEMM, one ascending-k chain per output;
+ * RNNB_BF16 / RNNB_TF32: tcgen05 with the recurrent layers' operand rounding.
+ * rnnb_linear_query what: 0 = 1 if the last forward ran on tcgen05,
+ * 1 = kernel launches of the last forward. */
+typedef struct rnnb_linear* rnnb_linear_t;
+rnnb_status rnnb_linear_create(rnnb_linear_t* out, int64_t d_in, int64_t d_out, int mode, int device);
+rnnb_status rnnb_linear_destroy(rnnb_linear_t h);
+rnnb_status rnnb_linear_set_weights(rnnb_linear_t h, const void* W, const void* bias, int src_dtype);
+rnnb_status rnnb_linear_forward(rnnb_linear_t h, const void* X, int64_t ldx, int64_t L, void* Y, int64_t ldy,
+                                void* stream);
+rnnb_status rnnb_linear_query(rnnb_linear_t h, int what, int64_t* value);
+
 /* Deterministic parameters of the reference's generators on the device:
  * elements offset .. offset+n-1 of the SplitMix64 stream of `seed`
  * (kernels.py:253-290) through the weight transform (u / 2^24) * 0.2 - 0.1

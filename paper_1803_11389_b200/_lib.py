@@ -27,6 +27,8 @@ SYMBOLS = (
     "rnnb_forward_ex", "rnnb_dev_alloc", "rnnb_dev_free", "rnnb_ipc_handle", "rnnb_ipc_open",
     "rnnb_ipc_close", "rnnb_peer_access", "rnnb_flag_signal", "rnnb_flag_wait",
     "rnnb_gemm", "rnnb_activation", "rnnb_splitmix_uniform",
+    "rnnb_linear_create", "rnnb_linear_destroy", "rnnb_linear_set_weights", "rnnb_linear_forward",
+    "rnnb_linear_query",
 )
 MAX_PEERS = 7
 IPC_HANDLE_BYTES = 64
@@ -89,6 +91,11 @@ def load():
         "rnnb_gemm": ([ci, vp, i64, vp, i64, vp, i64, i64, i64, i64, ci, vp], ci),
         "rnnb_activation": ([ci, vp, vp, i64, ci, vp], ci),
         "rnnb_splitmix_uniform": ([ctypes.c_uint64, ctypes.c_uint64, i64, vp, ci, vp], ci),
+        "rnnb_linear_create": ([ctypes.POINTER(vp), i64, i64, ci, ci], ci),
+        "rnnb_linear_destroy": ([vp], ci),
+        "rnnb_linear_set_weights": ([vp, vp, vp, ci], ci),
+        "rnnb_linear_forward": ([vp, vp, i64, i64, vp, i64, vp], ci),
+        "rnnb_linear_query": ([vp, ci, P64], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

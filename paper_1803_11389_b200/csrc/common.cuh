@@ -10,7 +10,9 @@
 
 namespace rnnb {
 
-enum Cell : int { SRU = 1, QRNN = 2 };
+// LINEAR: a dense layer Y = X W^T (+ b) on the same kernels (no gates, no
+// scan): the cfg3 acoustic model's input projection and logits
+enum Cell : int { SRU = 1, QRNN = 2, LINEAR = 3 };
 // Extra destinations of the last layer's h stores (peer GPUs' mapped buffers:
 // the pipeline hand-off / all-gather rides on the epilogue's stores).
 constexpr int kMaxPeers = 7;

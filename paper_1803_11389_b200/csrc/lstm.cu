@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/rnnb.h"
+#include "abi_guard.h"
 #include "common.cuh"
 
 namespace rnnb {
@@ -491,18 +492,6 @@ size_t es_of(int mode) { return mode == RNNB_F64 ? 8 : 4; }
     cudaError_t _e = (expr);                                                                  \
     if (_e != cudaSuccess) return set_error(RNNB_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
   } while (0)
-
-struct DeviceGuard {
-  int prev = 0;
-  bool switched = false;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) switched = cudaSetDevice(dev) == cudaSuccess;
-  }
-  ~DeviceGuard() {
-    if (switched) cudaSetDevice(prev);
-  }
-};
 
 size_t rec_smem(const rnnb_lstm* h, bool resident) {
   const size_t es = es_of(h->mode);

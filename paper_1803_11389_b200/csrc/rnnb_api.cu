@@ -1,4 +1,5 @@
 // C ABI of the blocked SRU/QRNN path (see include/rnnb.h).
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -6,6 +7,7 @@
 #include <vector>
 
 #include "../../include/rnnb.h"
+#include "abi_guard.h"
 #include "ffma_dispatch.cuh"
 #include "tc_dispatch.cuh"
 
@@ -96,6 +98,12 @@ struct rnnb_stack {
   int* stream_done = nullptr;
   int stream_chunk = 0;
   bool stream_refused = false;
+  // set after a streaming time-out (a serialising profiler, a stalled copy
+  // engine): later rnnb_forward_host calls on this handle use the chunked
+  // pipeline.  A handle is not meant for concurrent calls (the peer and
+  // streaming fields below are per call); the flag is atomic so a racing
+  // reader sees either value, never a torn one.
+  std::atomic<bool> stream_disabled{false};
   // rnnb_forward_ex: extra h destinations of the LAST layer (peer GPUs'
   // mapped buffers); cur_peers is non-zero only while that layer launches
   int n_peers = 0, cur_peers = 0;
@@ -105,7 +113,6 @@ struct rnnb_stack {
 namespace {
 
 constexpr int64_t kMaxStreamChunks = 64;
-bool g_stream_disabled = false;  // set after a streaming time-out (see rnnb_forward_host)
 
 // Stream memory operations (driver API, fetched through the runtime so the
 // library does not link libcuda): write a 32-bit value / wait for one.
@@ -448,7 +455,7 @@ rnnb_status rnnb_stack_create(rnnb_stack_t* out, int kind, int n_layers, const i
   return rnnb_stack_create_ex(out, kind, n_layers, d_in, d_h, mode, device, 0);
 }
 
-rnnb_status rnnb_stack_create_ex(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
+static rnnb_status rnnb_stack_create_ex_impl(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
                                  const int64_t* d_h, int mode, int device, int flags) {
   const bool wide = (flags & RNNB_FLAG_WIDE_SRU) != 0;
   if (!out) return fail(RNNB_EINVAL, "out is null");
@@ -488,11 +495,14 @@ rnnb_status rnnb_stack_create_ex(rnnb_stack_t* out, int kind, int n_layers, cons
   return RNNB_OK;
 }
 
+rnnb_status rnnb_stack_create_ex(rnnb_stack_t* out, int kind, int n_layers, const int64_t* d_in,
+                                 const int64_t* d_h, int mode, int device, int flags) {
+  return abi_guard("rnnb_stack_create_ex", [&]() { return rnnb_stack_create_ex_impl(out, kind, n_layers, d_in, d_h, mode, device, flags); });
+}
+
 rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   if (!h) return RNNB_OK;
-  int cur = 0;
-  cudaGetDevice(&cur);
-  cudaSetDevice(h->device);
+  DeviceGuard dg(h->device);
   for (auto& ly : h->layers) {
     if (ly.W) cudaFree(ly.W);
     if (ly.Wst) cudaFree(ly.Wst);
@@ -513,12 +523,11 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   if (h->stream_flag_host) cudaFreeHost(h->stream_flag_host);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->s_out) cudaStreamDestroy(h->s_out);
-  cudaSetDevice(cur);
   delete h;
   return RNNB_OK;
 }
 
-rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* mats, int n_mats, int src_dtype) {
+static rnnb_status rnnb_stack_set_layer_impl(rnnb_stack_t h, int layer, const void* const* mats, int n_mats, int src_dtype) {
   if (!h) return fail(RNNB_EINVAL, "null stack handle");
   if (layer < 0 || layer >= h->n_layers) return fail(RNNB_EINVAL, "layer index out of range");
   const int need = h->kind == RNNB_SRU ? 5 : 6;
@@ -554,9 +563,8 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
           }
         }
       }
-  int cur = 0;
-  cudaGetDevice(&cur);
-  CUDA_TRY(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
+  CUDA_TRY(dg.err);
   if (ly.W) cudaFree(ly.W), ly.W = nullptr;
   if (ly.Wst) cudaFree(ly.Wst), ly.Wst = nullptr;  // rebuilt from the new weights on first use
   if (ly.bias) cudaFree(ly.bias), ly.bias = nullptr;
@@ -618,8 +626,11 @@ rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* m
     }
   }
   ly.loaded = true;
-  cudaSetDevice(cur);
   return RNNB_OK;
+}
+
+rnnb_status rnnb_stack_set_layer(rnnb_stack_t h, int layer, const void* const* mats, int n_mats, int src_dtype) {
+  return abi_guard("rnnb_stack_set_layer", [&]() { return rnnb_stack_set_layer_impl(h, layer, mats, n_mats, src_dtype); });
 }
 
 rnnb_status rnnb_stack_set_highway(rnnb_stack_t h, int layer, int64_t col_offset) {
@@ -669,9 +680,8 @@ static rnnb_status forward_impl(rnnb_stack_t h, const void* X, int64_t ldx, int6
   if (!X || !H) return fail(RNNB_EINVAL, "null X or H");
   if (ldx < h->layers[0].din) return fail(RNNB_EINVAL, "ldx smaller than d_in");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int cur = 0;
-  cudaGetDevice(&cur);
-  if (cur != h->device) CUDA_TRY(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
+  CUDA_TRY(dg.err);
   switch (h->mode) {
     case RNNB_F64:
       st = forward_t<double, double>(h, static_cast<const double*>(X), ldx, L, block_size,
@@ -687,11 +697,10 @@ static rnnb_status forward_impl(rnnb_stack_t h, const void* X, int64_t ldx, int6
       st = forward_t<float, float>(h, static_cast<const float*>(X), ldx, L, block_size, static_cast<float*>(H),
                                    ldh, static_cast<float*>(c_state), static_cast<float*>(x_carry), s);
   }
-  if (cur != h->device) cudaSetDevice(cur);
   return st;
 }
 
-rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t block_size, void* H,
+static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t L, int64_t block_size, void* H,
                               void* c_state, void* x_carry, void* stream) {
   rnnb_status st = check_stack(h);
   if (st != RNNB_OK) return st;
@@ -704,9 +713,8 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
   const size_t xb = (size_t)L * din * es, hb = (size_t)L * dh * es;
   const size_t sb = (size_t)(csz + xsz) * es;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  int cur = 0;
-  cudaGetDevice(&cur);
-  if (cur != h->device) CUDA_TRY(cudaSetDevice(h->device));
+  DeviceGuard dg(h->device);
+  CUDA_TRY(dg.err);
   if (h->hx_bytes < xb + sb) {
     if (h->hostX) cudaFree(h->hostX);
     h->hostX = nullptr;
@@ -749,7 +757,7 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
   // drains chunk i while later chunks compute.
   const char* env_s = getenv("RNNB_HOST_STREAM");
   const bool want_stream =
-      !g_stream_disabled && !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
+      !h->stream_disabled.load() && !(env_s && env_s[0] == '0') && h->n_layers == 1 && h->mode == RNNB_F32;
   StreamOps so = stream_ops();
   if (want_stream && so.write && so.wait) {
     // The kernel counts finished h rows per granule g (whole blocks, >= 32
@@ -822,19 +830,14 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
           if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
           if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
           CUDA_TRY(cudaStreamSynchronize(s));
-          if (cur != h->device) cudaSetDevice(cur);
           return st;
         }
         // the rows did not arrive while the kernel waited (a serialising
         // profiler, a stalled copy engine): redo the call without streaming
-        if (cur != h->device) cudaSetDevice(cur);
-        g_stream_disabled = true;  // do not try streaming again in this process
-        return rnnb_forward_host(h, X, L, block_size, H, c_state, x_carry, stream);
+        h->stream_disabled.store(true);  // do not try streaming again with this handle
+        return rnnb_forward_host_impl(h, X, L, block_size, H, c_state, x_carry, stream);
       }
-      if (!h->stream_refused) {
-        if (cur != h->device) cudaSetDevice(cur);
-        return st;
-      }
+      if (!h->stream_refused) return st;
       st = RNNB_OK;  // the layer cannot stream: chunked pipeline below
     }
   }
@@ -875,8 +878,12 @@ rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t 
     if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
   }
   CUDA_TRY(cudaStreamSynchronize(s));
-  if (cur != h->device) cudaSetDevice(cur);
   return st;
+}
+
+rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t block_size, void* H,
+                              void* c_state, void* x_carry, void* stream) {
+  return abi_guard("rnnb_forward_host", [&]() { return rnnb_forward_host_impl(h, X, L, block_size, H, c_state, x_carry, stream); });
 }
 
 rnnb_status rnnb_gates(rnnb_stack_t h, int layer, const void* Xt, int64_t ldx, int64_t l, const void* x_carry,
@@ -890,6 +897,8 @@ rnnb_status rnnb_gates(rnnb_stack_t h, int layer, const void* Xt, int64_t ldx, i
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const Layer& ly = h->layers[layer];
   if (ldx < ly.din) return fail(RNNB_EINVAL, "ldx smaller than d_in");
+  DeviceGuard dg(h->device);
+  CUDA_TRY(dg.err);
   switch (h->mode) {
     case RNNB_F64:
       return layer_launch<double, double>(h, layer, static_cast<const double*>(Xt), ldx, l, l, nullptr, 0, nullptr,

@@ -17,10 +17,7 @@
 #include <vector>
 
 #include "../../include/rnnb.h"
-
-namespace rnnb {
-rnnb_status set_error(rnnb_status s, const std::string& msg);  // rnnb_api.cu
-}
+#include "abi_guard.h"
 
 namespace {
 
@@ -56,7 +53,25 @@ struct LayerDims {
   int64_t d_in, d_h;
 };
 
-// Canonical per-layer array sizes (model_io.py:133-139)
+// Payload bytes of one layer, or -1 when they exceed `limit` (the bytes left
+// in the file).  The header fields are untrusted u32s: d_h * d_in alone can
+// reach 2^64, so the arithmetic is done in 128 bits and compared with the
+// limit before anything is sized from it (model_io.py:246-248: a lying
+// header must fail as truncated, never trigger a huge allocation).
+int64_t layer_bytes_capped(int kind, int64_t din, int64_t dh, int es, int64_t limit) {
+  using u128 = unsigned __int128;
+  const u128 mat = (u128)(uint64_t)din * (u128)(uint64_t)dh;
+  const u128 vec = (u128)(uint64_t)dh;
+  u128 n;
+  if (kind == 0) n = 4 * mat + 4 * (u128)(uint64_t)dh * (u128)(uint64_t)dh + 4 * vec;  // LSTM
+  else if (kind == 1) n = 3 * mat + 2 * vec;                                            // SRU
+  else n = 6 * mat;                                                                      // QRNN
+  const u128 bytes = n * (u128)es;
+  return bytes > (u128)(limit < 0 ? 0 : limit) ? -1 : (int64_t)bytes;
+}
+
+// Canonical per-layer array sizes (model_io.py:133-139); only called once
+// layer_bytes_capped has bounded the products
 void layer_spec(int kind, int64_t din, int64_t dh, std::vector<int64_t>& sizes) {
   sizes.clear();
   if (kind == 0) {  // LSTM
@@ -101,13 +116,12 @@ rnnb_status parse_rnnw(const char* path, int* kind, int* prec, std::vector<Layer
     if (prev_dh >= 0 && din != prev_dh)
       return ferr("ShapeConsistencyError", lname + " input width does not match previous layer width");
     prev_dh = dh;
-    layer_spec(k, din, dh, sizes);
-    int64_t n = 0;
-    for (int64_t s : sizes) n += s;
-    if (file.remaining() < n * es) return ferr("TruncatedFileError", lname + " payload incomplete");
+    const int64_t nbytes = layer_bytes_capped(k, din, dh, es, file.remaining());
+    if (nbytes < 0) return ferr("TruncatedFileError", lname + " payload incomplete");
+    const int64_t n = nbytes / es;
     if (dims) dims->push_back({din, dh});
     if (payload) {
-      std::vector<unsigned char> raw((size_t)(n * es));
+      std::vector<unsigned char> raw((size_t)nbytes);
       if (!file.read(raw.data(), raw.size())) return ferr("TruncatedFileError", lname + " data");
       std::vector<double> vals((size_t)n);
       for (int64_t i = 0; i < n; ++i) {
@@ -148,161 +162,172 @@ extern "C" {
 
 rnnb_status rnnb_rnnw_info(const char* path, int* kind, int* precision, int* n_layers, int64_t* d_in, int64_t* d_h,
                            int max_layers) {
-  if (!kind || !precision || !n_layers) return set_error(RNNB_EINVAL, "null output argument");
-  std::vector<LayerDims> dims;
-  int k = 0, p = 0;
-  rnnb_status st = parse_rnnw(path, &k, &p, &dims, nullptr);
-  if (st != RNNB_OK) return st;
-  *kind = k;
-  *precision = p;
-  *n_layers = (int)dims.size();
-  for (int i = 0; i < (int)dims.size() && i < max_layers; ++i) {
-    if (d_in) d_in[i] = dims[(size_t)i].d_in;
-    if (d_h) d_h[i] = dims[(size_t)i].d_h;
-  }
-  return RNNB_OK;
+  return rnnb::abi_guard("rnnb_rnnw_info", [&]() -> rnnb_status {
+    if (!kind || !precision || !n_layers) return set_error(RNNB_EINVAL, "null output argument");
+    std::vector<LayerDims> dims;
+    int k = 0, p = 0;
+    rnnb_status st = parse_rnnw(path, &k, &p, &dims, nullptr);
+    if (st != RNNB_OK) return st;
+    *kind = k;
+    *precision = p;
+    *n_layers = (int)dims.size();
+    for (int i = 0; i < (int)dims.size() && i < max_layers; ++i) {
+      if (d_in) d_in[i] = dims[(size_t)i].d_in;
+      if (d_h) d_h[i] = dims[(size_t)i].d_h;
+    }
+    return RNNB_OK;
+  });
 }
 
 rnnb_status rnnb_stack_load_rnnw(rnnb_stack_t* out, const char* path, int mode, int device) {
-  if (!out) return set_error(RNNB_EINVAL, "null output handle");
-  *out = nullptr;
-  std::vector<LayerDims> dims;
-  std::vector<std::vector<double>> payload;
-  int k = 0, p = 0;
-  rnnb_status st = parse_rnnw(path, &k, &p, &dims, &payload);
-  if (st != RNNB_OK) return st;
-  if (k == 0) return set_error(RNNB_EINVAL, "blocked execution covers SRU and QRNN; use rnnb_lstm_load_rnnw for LSTM");
-  const int n = (int)dims.size();
-  std::vector<int64_t> din(n), dh(n);
-  for (int i = 0; i < n; ++i) din[i] = dims[i].d_in, dh[i] = dims[i].d_h;
-  rnnb_stack_t h = nullptr;
-  st = rnnb_stack_create(&h, k, n, din.data(), dh.data(), mode, device);
-  if (st != RNNB_OK) return st;
-  for (int li = 0; li < n; ++li) {
-    std::vector<const void*> mats = layer_ptrs(k, dims[(size_t)li], payload[(size_t)li]);
-    st = rnnb_stack_set_layer(h, li, mats.data(), (int)mats.size(), RNNB_DT_F64);
-    if (st != RNNB_OK) {
-      rnnb_stack_destroy(h);
-      return st;
+  return rnnb::abi_guard("rnnb_stack_load_rnnw", [&]() -> rnnb_status {
+    if (!out) return set_error(RNNB_EINVAL, "null output handle");
+    *out = nullptr;
+    std::vector<LayerDims> dims;
+    std::vector<std::vector<double>> payload;
+    int k = 0, p = 0;
+    rnnb_status st = parse_rnnw(path, &k, &p, &dims, &payload);
+    if (st != RNNB_OK) return st;
+    if (k == 0) return set_error(RNNB_EINVAL, "blocked execution covers SRU and QRNN; use rnnb_lstm_load_rnnw for LSTM");
+    const int n = (int)dims.size();
+    std::vector<int64_t> din(n), dh(n);
+    for (int i = 0; i < n; ++i) din[i] = dims[i].d_in, dh[i] = dims[i].d_h;
+    rnnb_stack_t h = nullptr;
+    st = rnnb_stack_create(&h, k, n, din.data(), dh.data(), mode, device);
+    if (st != RNNB_OK) return st;
+    for (int li = 0; li < n; ++li) {
+      std::vector<const void*> mats = layer_ptrs(k, dims[(size_t)li], payload[(size_t)li]);
+      st = rnnb_stack_set_layer(h, li, mats.data(), (int)mats.size(), RNNB_DT_F64);
+      if (st != RNNB_OK) {
+        rnnb_stack_destroy(h);
+        return st;
+      }
     }
-  }
-  *out = h;
-  return RNNB_OK;
+    *out = h;
+    return RNNB_OK;
+  });
 }
 
 rnnb_status rnnb_lstm_load_rnnw(rnnb_lstm_t* out, const char* path, int layer, int mode, int device) {
-  if (!out) return set_error(RNNB_EINVAL, "null output handle");
-  *out = nullptr;
-  std::vector<LayerDims> dims;
-  std::vector<std::vector<double>> payload;
-  int k = 0, p = 0;
-  rnnb_status st = parse_rnnw(path, &k, &p, &dims, &payload);
-  if (st != RNNB_OK) return st;
-  if (k != 0) return set_error(RNNB_EINVAL, "file does not hold LSTM weights");
-  if (layer < 0 || layer >= (int)dims.size()) return set_error(RNNB_EINVAL, "layer index out of range");
-  const LayerDims& d = dims[(size_t)layer];
-  rnnb_lstm_t h = nullptr;
-  st = rnnb_lstm_create(&h, d.d_in, d.d_h, mode, device);
-  if (st != RNNB_OK) return st;
-  std::vector<const void*> mats = layer_ptrs(0, d, payload[(size_t)layer]);
-  st = rnnb_lstm_set_weights(h, mats.data(), (int)mats.size(), RNNB_DT_F64);
-  if (st != RNNB_OK) {
-    rnnb_lstm_destroy(h);
-    return st;
-  }
-  *out = h;
-  return RNNB_OK;
+  return rnnb::abi_guard("rnnb_lstm_load_rnnw", [&]() -> rnnb_status {
+    if (!out) return set_error(RNNB_EINVAL, "null output handle");
+    *out = nullptr;
+    std::vector<LayerDims> dims;
+    std::vector<std::vector<double>> payload;
+    int k = 0, p = 0;
+    rnnb_status st = parse_rnnw(path, &k, &p, &dims, &payload);
+    if (st != RNNB_OK) return st;
+    if (k != 0) return set_error(RNNB_EINVAL, "file does not hold LSTM weights");
+    if (layer < 0 || layer >= (int)dims.size()) return set_error(RNNB_EINVAL, "layer index out of range");
+    const LayerDims& d = dims[(size_t)layer];
+    rnnb_lstm_t h = nullptr;
+    st = rnnb_lstm_create(&h, d.d_in, d.d_h, mode, device);
+    if (st != RNNB_OK) return st;
+    std::vector<const void*> mats = layer_ptrs(0, d, payload[(size_t)layer]);
+    st = rnnb_lstm_set_weights(h, mats.data(), (int)mats.size(), RNNB_DT_F64);
+    if (st != RNNB_OK) {
+      rnnb_lstm_destroy(h);
+      return st;
+    }
+    *out = h;
+    return RNNB_OK;
+  });
 }
 
 rnnb_status rnnb_rnnx_info(const char* path, int* precision, int64_t* seq_len, int64_t* width) {
-  File file(path);
-  if (!file.f) return set_error(RNNB_EINVAL, std::string("cannot open ") + (path ? path : "(null)"));
-  unsigned char h[20];
-  if (!file.read(h, 20)) return ferr("TruncatedFileError", "file ends inside header");
-  if (std::memcmp(h, "RNNX", 4) != 0) return ferr("BadMagicError", "bad magic, expected 'RNNX'");
-  const uint32_t version = rd32(h + 4);
-  if (version != kVersion)
-    return ferr("UnsupportedVersionError", "format version " + std::to_string(version) + ", expected 1");
-  const int p = h[8];
-  const int64_t L = rd32(h + 12), W = rd32(h + 16);
-  if (p > 1) return ferr("ShapeConsistencyError", "unknown precision code " + std::to_string(p));
-  if (L < 1 || W < 1) return ferr("ShapeConsistencyError", "sequence dimensions must be >= 1");
-  const int64_t payload = L * W * (p == 1 ? 8 : 4);
-  const int64_t got = file.remaining();
-  if (got < payload) return ferr("TruncatedFileError", "payload incomplete");
-  if (got > payload) return ferr("ShapeConsistencyError", "trailing bytes after payload");
-  if (precision) *precision = p;
-  if (seq_len) *seq_len = L;
-  if (width) *width = W;
-  return RNNB_OK;
+  return rnnb::abi_guard("rnnb_rnnx_info", [&]() -> rnnb_status {
+    File file(path);
+    if (!file.f) return set_error(RNNB_EINVAL, std::string("cannot open ") + (path ? path : "(null)"));
+    unsigned char h[20];
+    if (!file.read(h, 20)) return ferr("TruncatedFileError", "file ends inside header");
+    if (std::memcmp(h, "RNNX", 4) != 0) return ferr("BadMagicError", "bad magic, expected 'RNNX'");
+    const uint32_t version = rd32(h + 4);
+    if (version != kVersion)
+      return ferr("UnsupportedVersionError", "format version " + std::to_string(version) + ", expected 1");
+    const int p = h[8];
+    const int64_t L = rd32(h + 12), W = rd32(h + 16);
+    if (p > 1) return ferr("ShapeConsistencyError", "unknown precision code " + std::to_string(p));
+    if (L < 1 || W < 1) return ferr("ShapeConsistencyError", "sequence dimensions must be >= 1");
+    // L, W < 2^32 each: L * W * 8 needs up to 67 bits, so compare in 128 bits
+    const unsigned __int128 payload = (unsigned __int128)(uint64_t)L * (uint64_t)W * (unsigned)(p == 1 ? 8 : 4);
+    const int64_t got = file.remaining();
+    if ((unsigned __int128)(got < 0 ? 0 : got) < payload) return ferr("TruncatedFileError", "payload incomplete");
+    if ((unsigned __int128)got > payload) return ferr("ShapeConsistencyError", "trailing bytes after payload");
+    if (precision) *precision = p;
+    if (seq_len) *seq_len = L;
+    if (width) *width = W;
+    return RNNB_OK;
+  });
 }
 
 rnnb_status rnnb_rnnx_load(const char* path, void* dst, int dst_dtype, int dst_on_device, void* stream) {
-  int p = 0;
-  int64_t L = 0, W = 0;
-  rnnb_status st = rnnb_rnnx_info(path, &p, &L, &W);
-  if (st != RNNB_OK) return st;
-  if (!dst) return set_error(RNNB_EINVAL, "null destination");
-  if (dst_dtype != RNNB_DT_F32 && dst_dtype != RNNB_DT_F64) return set_error(RNNB_EINVAL, "dst dtype must be f32 or f64");
-  File file(path);
-  std::fseek(file.f, 20, SEEK_SET);
-  const int64_t n = L * W;
-  const int ses = p == 1 ? 8 : 4, des = dst_dtype == RNNB_DT_F64 ? 8 : 4;
-  constexpr int64_t kPiece = 1 << 20;  // elements per piece
-  std::vector<unsigned char> raw((size_t)(kPiece * ses));
-  unsigned char* stage = nullptr;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaEvent_t done[2] = {nullptr, nullptr};
-  if (dst_on_device) {
-    if (cudaMallocHost(&stage, (size_t)(2 * kPiece * des)) != cudaSuccess)
-      return set_error(RNNB_ECUDA, "pinned staging allocation failed");
-    cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming);
-  }
-  auto cleanup = [&]() {
-    if (stage) cudaFreeHost(stage);
-    for (auto& e : done)
-      if (e) cudaEventDestroy(e);
-  };
-  int slot = 0;
-  for (int64_t i0 = 0, piece = 0; i0 < n; i0 += kPiece, ++piece, slot ^= 1) {
-    const int64_t m = (n - i0) < kPiece ? (n - i0) : kPiece;
-    if (!file.read(raw.data(), (size_t)(m * ses))) {
-      cleanup();
-      return ferr("TruncatedFileError", "payload incomplete");
-    }
-    unsigned char* outp = dst_on_device ? stage + (size_t)slot * kPiece * des
-                                        : static_cast<unsigned char*>(dst) + (size_t)i0 * des;
-    if (dst_on_device && piece >= 2) cudaEventSynchronize(done[slot]);  // the copy out of this slot is done
-    for (int64_t i = 0; i < m; ++i) {
-      double v;
-      if (ses == 8) {
-        std::memcpy(&v, &raw[(size_t)i * 8], 8);
-      } else {
-        float f;
-        std::memcpy(&f, &raw[(size_t)i * 4], 4);
-        v = f;
-      }
-      if (des == 8) {
-        std::memcpy(outp + (size_t)i * 8, &v, 8);
-      } else {
-        const float f = (float)v;
-        std::memcpy(outp + (size_t)i * 4, &f, 4);
-      }
-    }
+  return rnnb::abi_guard("rnnb_rnnx_load", [&]() -> rnnb_status {
+    int p = 0;
+    int64_t L = 0, W = 0;
+    rnnb_status st = rnnb_rnnx_info(path, &p, &L, &W);
+    if (st != RNNB_OK) return st;
+    if (!dst) return set_error(RNNB_EINVAL, "null destination");
+    if (dst_dtype != RNNB_DT_F32 && dst_dtype != RNNB_DT_F64) return set_error(RNNB_EINVAL, "dst dtype must be f32 or f64");
+    File file(path);
+    std::fseek(file.f, 20, SEEK_SET);
+    const int64_t n = L * W;
+    const int ses = p == 1 ? 8 : 4, des = dst_dtype == RNNB_DT_F64 ? 8 : 4;
+    constexpr int64_t kPiece = 1 << 20;  // elements per piece
+    std::vector<unsigned char> raw((size_t)(kPiece * ses));
+    unsigned char* stage = nullptr;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaEvent_t done[2] = {nullptr, nullptr};
     if (dst_on_device) {
-      cudaError_t e = cudaMemcpyAsync(static_cast<unsigned char*>(dst) + (size_t)i0 * des, outp, (size_t)(m * des),
-                                      cudaMemcpyHostToDevice, s);
-      if (e == cudaSuccess) e = cudaEventRecord(done[slot], s);
-      if (e != cudaSuccess) {
+      if (cudaMallocHost(&stage, (size_t)(2 * kPiece * des)) != cudaSuccess)
+        return set_error(RNNB_ECUDA, "pinned staging allocation failed");
+      cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming);
+    }
+    auto cleanup = [&]() {
+      if (stage) cudaFreeHost(stage);
+      for (auto& e : done)
+        if (e) cudaEventDestroy(e);
+    };
+    int slot = 0;
+    for (int64_t i0 = 0, piece = 0; i0 < n; i0 += kPiece, ++piece, slot ^= 1) {
+      const int64_t m = (n - i0) < kPiece ? (n - i0) : kPiece;
+      if (!file.read(raw.data(), (size_t)(m * ses))) {
         cleanup();
-        return set_error(RNNB_ECUDA, std::string("RNNX upload: ") + cudaGetErrorString(e));
+        return ferr("TruncatedFileError", "payload incomplete");
+      }
+      unsigned char* outp = dst_on_device ? stage + (size_t)slot * kPiece * des
+                                          : static_cast<unsigned char*>(dst) + (size_t)i0 * des;
+      if (dst_on_device && piece >= 2) cudaEventSynchronize(done[slot]);  // the copy out of this slot is done
+      for (int64_t i = 0; i < m; ++i) {
+        double v;
+        if (ses == 8) {
+          std::memcpy(&v, &raw[(size_t)i * 8], 8);
+        } else {
+          float f;
+          std::memcpy(&f, &raw[(size_t)i * 4], 4);
+          v = f;
+        }
+        if (des == 8) {
+          std::memcpy(outp + (size_t)i * 8, &v, 8);
+        } else {
+          const float f = (float)v;
+          std::memcpy(outp + (size_t)i * 4, &f, 4);
+        }
+      }
+      if (dst_on_device) {
+        cudaError_t e = cudaMemcpyAsync(static_cast<unsigned char*>(dst) + (size_t)i0 * des, outp, (size_t)(m * des),
+                                        cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaEventRecord(done[slot], s);
+        if (e != cudaSuccess) {
+          cleanup();
+          return set_error(RNNB_ECUDA, std::string("RNNX upload: ") + cudaGetErrorString(e));
+        }
       }
     }
-  }
-  if (dst_on_device) cudaStreamSynchronize(s);
-  cleanup();
-  return RNNB_OK;
+    if (dst_on_device) cudaStreamSynchronize(s);
+    cleanup();
+    return RNNB_OK;
+  });
 }
 
 }  // extern "C"

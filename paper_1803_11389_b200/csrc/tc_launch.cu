@@ -161,6 +161,12 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
   const int nitems = a.nU * a.nB;
   const int grid = nitems < num_sms ? nitems : num_sms;
   if (grid_out) *grid_out = grid;
+  if (cell == LINEAR) {
+    // dense layers: bf16 / tf32 products (fp32 layers run the FFMA kernel)
+    if (mode == TC_BF16) return run_n<LINEAR, TC_BF16>(N, a, tw, tx, grid, s);
+    if (mode == TC_TF32) return run_n<LINEAR, TC_TF32>(N, a, tw, tx, grid, s);
+    return cudaErrorInvalidValue;
+  }
   if (cell == SRU) {
     if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tw, tx, grid, s);
     if (mode == TC_TF32) return run_n<SRU, TC_TF32>(N, a, tw, tx, grid, s);

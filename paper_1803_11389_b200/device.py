@@ -197,6 +197,77 @@ class DeviceStack:
         self.close()
 
 
+class DeviceLinear:
+    """Dense layer Y = X W^T (+ b) resident on one GPU (include/rnnb.h
+    rnnb_linear_*): the cfg3 acoustic model's input projection and logits,
+    kernels.gemm(W, X^T) (kernels.py:203-225) in the time-major layout.
+    mode: "f32" / "f64" / "f32x3" (FFMA GEMM) or "bf16" / "tf32" (tcgen05)."""
+
+    def __init__(self, W, bias=None, mode="f32", device=None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _lib.RnnbError("CUDA is not available: the dense layers have no CPU fallback")
+        self.lib = _lib.load()
+        if mode not in _lib.MODES:
+            raise ValueError(f"mode must be one of {sorted(_lib.MODES)}")
+        self.mode = mode
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        src = np.float64 if mode == "f64" else np.float32
+        W = np.ascontiguousarray(np.asarray(W), dtype=src)
+        if W.ndim != 2:
+            raise ValueError("W must be a 2-d [d_out x d_in] array")
+        self.d_out, self.d_in = (int(v) for v in W.shape)
+        h = ctypes.c_void_p()
+        _lib.check(self.lib.rnnb_linear_create(ctypes.byref(h), self.d_in, self.d_out, _lib.MODES[mode],
+                                               self.device))
+        self._h = h
+        b = None if bias is None else np.ascontiguousarray(np.asarray(bias), dtype=src)
+        if b is not None and b.shape != (self.d_out,):
+            raise ValueError(f"bias must have shape ({self.d_out},)")
+        dt = _lib.DT_F64 if src is np.float64 else _lib.DT_F32
+        _lib.check(self.lib.rnnb_linear_set_weights(self._h, W.ctypes.data_as(ctypes.c_void_p),
+                                                    None if b is None else b.ctypes.data_as(ctypes.c_void_p), dt))
+
+    @property
+    def dtype(self):
+        torch = _torch()
+        return torch.float64 if self.mode == "f64" else torch.float32
+
+    def forward(self, X, out=None, stream=None):
+        """X [L x d_in] CUDA tensor -> [L x d_out]."""
+        torch = _torch()
+        if not isinstance(X, torch.Tensor) or not X.is_cuda or X.dim() != 2 or X.stride(1) != 1:
+            raise ValueError("X must be a 2-d row-major CUDA tensor")
+        if X.dtype != self.dtype:
+            raise ValueError(f"dtype mismatch: {X.dtype} vs {self.dtype}")
+        if X.device.index != self.device:
+            raise ValueError(f"X is on {X.device}, the layer on cuda:{self.device}")
+        if X.shape[1] != self.d_in:
+            raise ValueError(f"input must be [L x {self.d_in}], got {tuple(X.shape)}")
+        L = X.shape[0]
+        if out is None:
+            out = torch.empty((L, self.d_out), dtype=self.dtype, device=X.device)
+        _lib.check(self.lib.rnnb_linear_forward(self._h, ctypes.c_void_p(X.data_ptr()), X.stride(0), L,
+                                                ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_ptr(stream)))
+        return out
+
+    def query(self, what):
+        v = ctypes.c_int64()
+        _lib.check(self.lib.rnnb_linear_query(self._h, what, ctypes.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.lib.rnnb_linear_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DeviceLstm:
     """One LSTM layer resident on one GPU (lstm_run_precomputed,
     blocked.py:271-305): the input-side products for the sequence in one

@@ -345,6 +345,12 @@ class P2PBidirSRU(_PeerBuffers):
     def close_call(self):
         self.epoch += 1
 
+    def close(self):
+        super().close()
+        for per_dir in self.stages:
+            for st in per_dir:
+                st.close()
+
     def forward(self, X):
         """One process per GPU: the whole stack; returns [L x 2H]."""
         out = torch.empty((self.L, 2 * self.H), dtype=torch.float32, device=self.final.device)
