@@ -230,7 +230,11 @@ rnnb_status rnnb_rnnx_load(const char* path, void* dst, int dst_dtype, int dst_o
  * peer buffers: the next pipeline stage's input ring, or every rank's
  * all-gathered next-layer input).  ldh may be negative (|ldh| >= d_h): rows
  * are then stored in reverse time order (the backward direction of a
- * bidirectional layer writes its reversed output in place). */
+ * bidirectional layer writes its reversed output in place).  ldx may be
+ * negative too (|ldx| >= d_in, X = address of time step 0): the backward
+ * direction then reads the forward-ordered input in reverse without a
+ * copy on the tensor-core path (its operand conversion walks the rows
+ * backwards); the FFMA paths make one reversed copy with an own kernel. */
 #define RNNB_MAX_PEERS 7
 rnnb_status rnnb_forward_ex(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, int64_t block_size,
                             void* H, int64_t ldh, void* c_state, void* x_carry, int n_peers,

@@ -76,6 +76,8 @@ struct rnnb_stack {
   void* ws[2] = {nullptr, nullptr};
   size_t ws_bytes = 0;
   int64_t last_launches = 0;
+  void* rev = nullptr;    // time-reversed copy of the input for the FFMA paths (ldx < 0), [L][d_in]
+  size_t rev_bytes = 0;
   void* op = nullptr;     // tensor-core operand copy of a layer input, [L+1][maxD]
   size_t op_bytes = 0;
   float* cbuf = nullptr;  // tensor-core c_T scratch + look-back state + status words
@@ -366,9 +368,42 @@ rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_
   return RNNB_OK;
 }
 
+// Rows of a time-reversed input view (row t at X + t*ldx, ldx < 0) into a
+// dense [L][D] buffer, 16-byte vectors when aligned.
+template <typename T>
+__global__ void reverse_rows_kernel(const T* __restrict__ X, int64_t ldx, T* __restrict__ out, int64_t L, int D) {
+  for (int64_t r = blockIdx.y; r < L; r += gridDim.y) {
+    const T* src = X + r * ldx;
+    T* dst = out + r * D;
+    for (int d = blockIdx.x * blockDim.x + threadIdx.x; d < D; d += gridDim.x * blockDim.x) dst[d] = src[d];
+  }
+}
+
 template <typename TA, typename TW>
 rnnb_status forward_t(rnnb_stack* h, const TA* X, int64_t ldx, int64_t L, int64_t Tb, TA* H,
                       int64_t ldh, TA* c_state, TA* x_carry, cudaStream_t s) {
+  if (ldx < 0 && !(sizeof(TA) == 4 && use_tc(h, Tb))) {
+    // Time-reversed input (the backward direction of a bidirectional stack).
+    // The tcgen05 path reads it directly: its operand conversion walks the
+    // rows with the negative stride.  The FFMA kernels fetch x with TMA
+    // boxes, whose strides are unsigned, so they get a dense reversed copy.
+    const int64_t din = h->layers[0].din;
+    const size_t rb = (size_t)L * din * sizeof(TA);
+    if (h->rev_bytes < rb) {
+      if (h->rev) cudaFree(h->rev);
+      h->rev = nullptr;
+      h->rev_bytes = 0;
+      CUDA_TRY(cudaMalloc(&h->rev, rb));
+      h->rev_bytes = rb;
+    }
+    const int bx = (int)((din + 255) / 256);
+    const int by = (int)(L < 4096 ? L : 4096);
+    reverse_rows_kernel<TA><<<dim3(bx, by), 256, 0, s>>>(X, ldx, static_cast<TA*>(h->rev), L, (int)din);
+    CUDA_TRY(cudaGetLastError());
+    rnnb_status st = forward_t<TA, TW>(h, static_cast<const TA*>(h->rev), din, L, Tb, H, ldh, c_state, x_carry, s);
+    h->last_launches += 1;
+    return st;
+  }
   int64_t maxw = 0;
   for (auto& ly : h->layers) maxw = ly.dh > maxw ? ly.dh : maxw;
   if (h->n_layers > 1) {
@@ -511,6 +546,7 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
     if (ly.bias_tc) cudaFree(ly.bias_tc);
   }
   if (h->op) cudaFree(h->op);
+  if (h->rev) cudaFree(h->rev);
   if (h->cbuf) cudaFree(h->cbuf);
   if (h->tc_status) cudaFree(h->tc_status);
   for (auto& p : h->ws)
@@ -678,7 +714,8 @@ static rnnb_status forward_impl(rnnb_stack_t h, const void* X, int64_t ldx, int6
   if (L < 1) return fail(RNNB_EINVAL, "seq_len must be >= 1");
   if (block_size < 1) return fail(RNNB_EINVAL, "block_size must be >= 1");
   if (!X || !H) return fail(RNNB_EINVAL, "null X or H");
-  if (ldx < h->layers[0].din) return fail(RNNB_EINVAL, "ldx smaller than d_in");
+  // ldx < 0: rows in reverse time order (row t at X + t*ldx)
+  if ((ldx < 0 ? -ldx : ldx) < h->layers[0].din) return fail(RNNB_EINVAL, "|ldx| smaller than d_in");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   DeviceGuard dg(h->device);
   CUDA_TRY(dg.err);

@@ -325,6 +325,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int s = it % C::STAGES;
           mbar_wait_sleep(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
+          if (a.dbg & 128) {  // timing experiment: no loads (MMAs read stale tiles)
+            mbar_arrive(&full[s]);
+            continue;
+          }
           mbar_arrive_expect_tx(&full[s], C::STAGE_BYTES);
           const int tap = kt >= a.nKtap ? 1 : 0;
           const int kx = (kt - tap * a.nKtap) * C::KT;
@@ -366,7 +370,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint64_t bdesc0 = sw128_desc(st + 3 * C::A_BYTES);
           constexpr int HALF = 3 * C::A_BYTES + C::B_BYTES;
 #pragma unroll
-          for (int g = 0; g < 3; ++g) {
+          for (int g = 0; g < ((a.dbg & 64) ? 0 : 3); ++g) {  // dbg 64 (timing): no MMAs
             const uint64_t adesc0 = sw128_desc(st + g * C::A_BYTES);
 #pragma unroll
             for (int kk = 0; kk < C::KT / C::UK; ++kk) {
@@ -413,6 +417,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int64_t t0 = (int64_t)b * a.T_b;
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       const int unit = u * 128 + row;
+      if (a.dbg & 32) {  // timing experiment: epilogue only hands the accumulators back
+        const int nacc = C::CHUNKED ? (a.nK + C::CK - 1) / C::CK : 1;
+        for (int ch = 0; ch < nacc; ++ch, ++acc_it) {
+          const int ab = acc_it % C::NACC;
+          mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
+          tc_fence_after();
+          tc_fence_before();
+          mbar_arrive(&acc_empty[ab]);
+        }
+        continue;
+      }
       if constexpr (CELL == LINEAR) {
         // dense layer: gate plane g holds output columns [g*Hpad, (g+1)*Hpad);
         // accumulators + bias straight to Y (a warp stores 128 contiguous bytes per row)

@@ -106,10 +106,33 @@ class DeviceStack:
         torch = _torch()
         if not isinstance(t, torch.Tensor) or not t.is_cuda:
             raise ValueError(f"{name} must be a CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{name} is on {t.device}, the stack on cuda:{self.device}")
         if t.dtype != self.dtype:
             raise ValueError(f"dtype mismatch: {t.dtype} vs {self.dtype}")
         if t.dim() != 2 or t.stride(1) != 1:
             raise ValueError(f"{name} must be a 2-d row-major tensor")
+
+    def _check_state(self, t, n, name, host=False):
+        """c_state / x_carry: exactly n elements of the stack's dtype, contiguous,
+        on the stack's device (or host arrays for forward_host): the kernels
+        read and write n elements through the pointer."""
+        if t is None:
+            return None
+        if host:
+            if not isinstance(t, np.ndarray) or t.dtype != self.np_dtype or t.size != n or not t.flags.c_contiguous:
+                raise ValueError(f"{name} must be a contiguous {np.dtype(self.np_dtype).name} array of {n} elements")
+            return t.ctypes.data_as(ctypes.c_void_p)
+        torch = _torch()
+        if not isinstance(t, torch.Tensor) or not t.is_cuda:
+            raise ValueError(f"{name} must be a CUDA tensor")
+        if t.dtype != self.dtype:
+            raise ValueError(f"{name} dtype mismatch: {t.dtype} vs {self.dtype}")
+        if t.numel() != n or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous tensor of {n} elements, got {tuple(t.shape)}")
+        if t.device.index != self.device:
+            raise ValueError(f"{name} is on {t.device}, the stack on cuda:{self.device}")
+        return ctypes.c_void_p(t.data_ptr())
 
     def forward(self, X, block_size, out=None, c_state=None, x_carry=None, stream=None):
         """run_blocked on device tensors; X [L x d_in] -> [L x d_h]."""
@@ -121,8 +144,10 @@ class DeviceStack:
         if out is None:
             out = torch.empty((L, self.d_h[-1]), dtype=self.dtype, device=X.device)
         self._check_dev(out, "out")
-        cp = ctypes.c_void_p(c_state.data_ptr()) if c_state is not None else None
-        xp = ctypes.c_void_p(x_carry.data_ptr()) if x_carry is not None else None
+        if out.shape != (L, self.d_h[-1]):
+            raise ValueError(f"out must be [{L} x {self.d_h[-1]}], got {tuple(out.shape)}")
+        cp = self._check_state(c_state, sum(self.d_h), "c_state")
+        xp = self._check_state(x_carry, sum(self.d_in), "x_carry")
         _lib.check(self.lib.rnnb_forward(self._h, ctypes.c_void_p(X.data_ptr()), X.stride(0), L,
                                          int(block_size), ctypes.c_void_p(out.data_ptr()),
                                          out.stride(0), cp, xp, _stream_ptr(stream)))
@@ -135,8 +160,8 @@ class DeviceStack:
         buffers; ldh < 0 stores rows in reverse time order)."""
         peers = [int(p) for p in peers]
         arr = (ctypes.c_void_p * max(1, len(peers)))(*peers) if peers else None
-        cp = ctypes.c_void_p(c_state.data_ptr()) if c_state is not None else None
-        xp = ctypes.c_void_p(x_carry.data_ptr()) if x_carry is not None else None
+        cp = self._check_state(c_state, sum(self.d_h), "c_state")
+        xp = self._check_state(x_carry, sum(self.d_in), "x_carry")
         _lib.check(self.lib.rnnb_forward_ex(self._h, ctypes.c_void_p(int(x_ptr)), int(ldx), int(L), int(block_size),
                                             ctypes.c_void_p(int(h_ptr)), int(ldh), cp, xp, len(peers), arr,
                                             _stream_ptr(stream)))
@@ -148,8 +173,11 @@ class DeviceStack:
             raise ValueError(f"input must be [L x {self.d_in[0]}], got {X.shape}")
         if out is None:
             out = np.empty((X.shape[0], self.d_h[-1]), self.np_dtype)
-        cp = c_state.ctypes.data_as(ctypes.c_void_p) if c_state is not None else None
-        xp = x_carry.ctypes.data_as(ctypes.c_void_p) if x_carry is not None else None
+        elif (not isinstance(out, np.ndarray) or out.dtype != self.np_dtype or not out.flags.c_contiguous
+              or out.shape != (X.shape[0], self.d_h[-1])):
+            raise ValueError(f"out must be a contiguous [{X.shape[0]} x {self.d_h[-1]}] array")
+        cp = self._check_state(c_state, sum(self.d_h), "c_state", host=True)
+        xp = self._check_state(x_carry, sum(self.d_in), "x_carry", host=True)
         _lib.check(self.lib.rnnb_forward_host(self._h, X.ctypes.data_as(ctypes.c_void_p), X.shape[0],
                                               int(block_size), out.ctypes.data_as(ctypes.c_void_p),
                                               cp, xp, _stream_ptr(stream)))
@@ -317,8 +345,20 @@ class DeviceLstm:
         if X.shape[1] != self.d_in:
             raise ValueError(f"input must be [L x {self.d_in}], got {tuple(X.shape)}")
         L = X.shape[0]
+        if X.device.index != self.device:
+            raise ValueError(f"X is on {X.device}, the layer on cuda:{self.device}")
         if out is None:
             out = torch.empty((L, self.d_h), dtype=self.dtype, device=X.device)
+        for t, name in ((out, "out"), (c_state, "c_state"), (h_state, "h_state")):
+            if t is None:
+                continue
+            if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != self.dtype or t.device.index != self.device:
+                raise ValueError(f"{name} must be a {self.dtype} tensor on cuda:{self.device}")
+        if out.shape != (L, self.d_h) or out.stride(1) != 1:
+            raise ValueError(f"out must be a row-major [{L} x {self.d_h}] tensor")
+        for t, name in ((c_state, "c_state"), (h_state, "h_state")):
+            if t is not None and (t.numel() != self.d_h or not t.is_contiguous()):
+                raise ValueError(f"{name} must be a contiguous tensor of {self.d_h} elements")
         cp = ctypes.c_void_p(c_state.data_ptr()) if c_state is not None else None
         hp = ctypes.c_void_p(h_state.data_ptr()) if h_state is not None else None
         _lib.check(self.lib.rnnb_lstm_forward(self._h, ctypes.c_void_p(X.data_ptr()), X.stride(0), L,
@@ -332,6 +372,10 @@ class DeviceLstm:
             raise ValueError(f"input must be [L x {self.d_in}], got {X.shape}")
         if out is None:
             out = np.empty((X.shape[0], self.d_h), self.np_dtype)
+        for t, name in ((c_state, "c_state"), (h_state, "h_state")):
+            if t is not None and (not isinstance(t, np.ndarray) or t.dtype != self.np_dtype or t.size != self.d_h
+                                  or not t.flags.c_contiguous):
+                raise ValueError(f"{name} must be a contiguous {np.dtype(self.np_dtype).name} array of {self.d_h}")
         cp = c_state.ctypes.data_as(ctypes.c_void_p) if c_state is not None else None
         hp = h_state.ctypes.data_as(ctypes.c_void_p) if h_state is not None else None
         _lib.check(self.lib.rnnb_lstm_forward_host(self._h, X.ctypes.data_as(ctypes.c_void_p), X.shape[0],

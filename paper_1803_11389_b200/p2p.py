@@ -279,9 +279,6 @@ class P2PBidirSRU(_PeerBuffers):
         self.act = torch.empty((2, seq_len, W), dtype=torch.float32, device=dev)
         self.final = torch.empty((seq_len, W), dtype=torch.float32, device=dev)
         self.flags = torch.zeros(2 * world * FLAG_STRIDE, dtype=torch.int32, device=dev)
-        # time-reversed copies of the layer inputs (backward direction)
-        self.xrev = {w: torch.empty((seq_len, w), dtype=torch.float32, device=dev) for w in {self.d_in0, W}}
-        self.rev_idx = torch.arange(seq_len - 1, -1, -1, device=dev)
         self.stream = stream if stream is not None else torch.cuda.Stream(device=dev)
         self.epoch = 0
         self.peer = None
@@ -331,12 +328,10 @@ class P2PBidirSRU(_PeerBuffers):
             if d == 0:  # forward direction: time order, columns [u0, u1)
                 col, row, ldh = self.u0, 0, W
                 xp, ldx = x.data_ptr(), x.stride(0)
-            else:  # backward: reversed input copy, negative-stride stores at [H + u0, H + u1)
-                xr = self.xrev[x.shape[1]]
-                with torch.cuda.stream(s):
-                    torch.index_select(x, 0, self.rev_idx, out=xr)
+            else:  # backward: the input read in reverse (negative row stride, no copy on the
+                # tensor-core path), negative-stride stores at [H + u0, H + u1)
                 col, row, ldh = H + self.u0, (L - 1) * W, -W
-                xp, ldx = xr.data_ptr(), xr.stride(0)
+                xp, ldx = x.data_ptr() + (L - 1) * x.stride(0) * x.element_size(), -x.stride(0)
             st.forward_ptr(xp, ldx, L, self.block_size, t.data_ptr() + (row + col) * 4, ldh,
                            peers=[self.peer[p][name] + (off + row + col) * 4 for p in others], stream=s)
         else:

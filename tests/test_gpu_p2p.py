@@ -214,3 +214,28 @@ def test_p2p_pipeline_ipc_two_processes(tmp_path, oracle):
     X = torch.from_numpy(np.random.default_rng(1).standard_normal((640, 128)).astype(np.float32)).cuda()
     ref = _chunked_reference(st, X, 64, 32).cpu().numpy()
     assert got.tobytes() == ref.tobytes()
+
+
+@pytest.mark.parametrize("mode,T_b", [("f32", 16), ("f32", 64), ("bf16", 16), ("bf16", 64), ("tf32", 32)])
+def test_negative_input_stride_reads_time_reversed(oracle, mode, T_b):
+    """rnnb_forward_ex with ldx < 0 (the bidirectional backward direction):
+    bitwise the forward over an explicitly flipped copy, on the tensor-core
+    path (operand conversion walks the rows backwards) and the FFMA path (one
+    reversed copy by an own kernel); QRNN x_carry = the last row READ."""
+    import torch
+    import paper_1803_11389_b200 as P
+    for kind in ("sru", "qrnn"):
+        layers = oracle.generate_layers(kind, 192, 192, 2, 31, np.float32)
+        X = torch.from_numpy(np.random.default_rng(4).standard_normal((203, 192)).astype(np.float32)).cuda()
+        st = P.DeviceStack(kind, layers, mode=mode)
+        flipped = torch.flip(X, dims=[0]).contiguous()
+        xc1 = torch.zeros(384, device="cuda")
+        want = st.forward(flipped, T_b, x_carry=xc1)
+        out = torch.empty_like(want)
+        xc2 = torch.zeros(384, device="cuda")
+        st.forward_ptr(X.data_ptr() + 202 * X.stride(0) * 4, -X.stride(0), 203, T_b, out.data_ptr(), out.stride(0),
+                       x_carry=xc2)
+        torch.cuda.synchronize()
+        assert out.cpu().numpy().tobytes() == want.cpu().numpy().tobytes(), (kind, mode)
+        assert torch.equal(xc1, xc2)
+        st.close()
