@@ -24,7 +24,8 @@
 // all CTAs co-resident the chain cannot deadlock.
 //
 // Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer (one elected lane), warps 2..5 epilogue (TMEM lane quadrant w%4).
+// issuer (the converged warp; elect.sync picks the issuing lane), warps 2..5
+// epilogue (TMEM lane quadrant w%4).
 #pragma once
 #include <cuda.h>
 
@@ -61,7 +62,8 @@ struct TcArgs {
   int nK;             // k-tiles per row (taps * Dp / KT)
   int nKtap;          // k-tiles per tap
   int nU, nB;
-  int dbg;            // RNNB_DEBUG bits (timing experiments): 16 = skip the c-chain wait
+  int dbg;            // RNNB_DEBUG bits, timing experiments only (results wrong): 16 no look-back,
+                      // 32 no epilogue, 64 no MMAs, 128 no loads, 512 no scan/stores, 1024 no activations
 };
 
 template <int MODE> struct TcT;
@@ -113,6 +115,58 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+// ---- one k-tile of MMAs as ONE asm block, executed by the whole (converged)
+// MMA warp with elect.sync inside: the descriptors are warp-uniform, so ptxas
+// issues the UTCHMMAs back to back from uniform registers.  Issued from a
+// lane-0-only branch, each MMA sat in an ELECT/BRA.U.ANY loop with dependent
+// uniform-register moves: 82 cycles per 128xNx16 MMA vs 56 this way
+// (tools/mma_rate.cu, profiles/mma_rate_r2.json; the hardware floor is ~51
+// cycles for any N <= 64).  Gate g: A tile a0 + g*16 KB, accumulator d0 + g*N;
+// K-step kk: start address + 32 B.  acc == 0 starts the accumulation.
+#define RNNB_MMA(KIND, ACCP) "@e tcgen05.mma.cta_group::1.kind::" KIND " [d], a, b, %3, " ACCP ";\n\t"
+#define RNNB_KSTEP(KIND) "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t" RNNB_MMA(KIND, "1")
+#define RNNB_GATE(KIND, G)                                                                        \
+  "add.s64 a, %1, " #G "*1024;\n\tmov.b64 b, %2;\n\tmad.lo.s32 d, %5, " #G ", %0;\n\t" RNNB_MMA(KIND, "p") \
+      RNNB_KSTEP(KIND) RNNB_KSTEP(KIND) RNNB_KSTEP(KIND)
+#define RNNB_KTILE(KIND)                                                                            \
+  "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t.reg .b32 d;\n\telect.sync _|e, 0xffffffff;\n\t" \
+  "setp.ne.b32 p, %4, 0;\n\t" RNNB_GATE(KIND, 0) RNNB_GATE(KIND, 1) RNNB_GATE(KIND, 2) "}\n"
+// 3xTF32: per K-step hi.hi (starts with acc), hi.lo, lo.hi; the lo planes sit
+// %6 (16-byte units) after the hi planes
+#define RNNB_X3STEP(ACCP)                                                                   \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, b, %3, " ACCP ";\n\t"                    \
+  "add.s64 bl, b, %6;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, bl, %3, 1;\n\t"   \
+  "add.s64 al, a, %6;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [d], al, b, %3, 1;\n\t"
+#define RNNB_X3NEXT "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t" RNNB_X3STEP("1")
+#define RNNB_X3GATE(G) \
+  "add.s64 a, %1, " #G "*1024;\n\tmov.b64 b, %2;\n\tmad.lo.s32 d, %5, " #G ", %0;\n\t" RNNB_X3STEP("p") RNNB_X3NEXT RNNB_X3NEXT RNNB_X3NEXT
+template <int MODE>
+__device__ __forceinline__ void tc_issue_ktile(uint32_t d0, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc,
+                                               uint32_t n, uint64_t lo16) {
+  if constexpr (MODE == TC_BF16)
+    asm volatile(RNNB_KTILE("f16") ::"r"(d0), "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n), "l"(lo16));
+  else if constexpr (MODE == TC_TF32)
+    asm volatile(RNNB_KTILE("tf32") ::"r"(d0), "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n), "l"(lo16));
+  else
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b, al, bl;\n\t.reg .b32 d;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t" RNNB_X3GATE(0) RNNB_X3GATE(1) RNNB_X3GATE(2) "}\n" ::"r"(d0),
+        "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n), "l"(lo16));
+}
+#undef RNNB_MMA
+#undef RNNB_KSTEP
+#undef RNNB_GATE
+#undef RNNB_KTILE
+#undef RNNB_X3STEP
+#undef RNNB_X3NEXT
+#undef RNNB_X3GATE
+// tcgen05.commit from the converged MMA warp, one elected lane
+__device__ __forceinline__ void tc_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const float (&v)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
@@ -135,6 +189,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// tcgen05.ld without the wait: issue several, then one tmem_wait_ld() and a
+// reg_fence per destination array (the empty volatile asm "redefines" the
+// registers after the wait, so no use can be scheduled before it)
+__device__ __forceinline__ void tmem_ld16_raw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void reg_fence(uint32_t (&r)[16]) {
+  asm volatile(""
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                 "+r"(r[15]));
+}
+// the three gate accumulators of 16 columns, one wait
+__device__ __forceinline__ void tmem_ld_gates16(uint32_t tz, uint32_t tf, uint32_t to, float (&z)[16], float (&f)[16],
+                                                float (&o)[16]) {
+  uint32_t rz[16], rf[16], ro[16];
+  tmem_ld16_raw(tz, rz);
+  tmem_ld16_raw(tf, rf);
+  tmem_ld16_raw(to, ro);
+  tmem_wait_ld();
+  reg_fence(rz);
+  reg_fence(rf);
+  reg_fence(ro);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    z[i] = __uint_as_float(rz[i]);
+    f[i] = __uint_as_float(rf[i]);
+    o[i] = __uint_as_float(ro[i]);
+  }
 }
 
 // K-major, 128-byte-swizzled operand tile (rows of 128 B, 8-row atoms 1 KB apart)
@@ -215,13 +305,11 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
   a.aggA[sidx] = Ablk;
   a.aggB[sidx] = Bblk;
   // the barrier orders the 128 threads' stores before thread 0's gpu-scope
-  // fence + release (cumulativity), one fence per item instead of 128
+  // release (st.release = fence.acq_rel.gpu + store; cumulative over the
+  // writes the barrier ordered before it), one fence per item instead of 128
   tc_epi_sync();
   const int tag = 4 * a.epoch;
-  if (et == 0) {
-    __threadfence();
-    st_release(&a.status[(size_t)b * a.nU + u], tag + 1);
-  }
+  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 1);
   const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
   // lanes of the first epilogue warp wait for the statuses in parallel
   if (et < 32) {
@@ -231,22 +319,34 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
     if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < tag + 2) __nanosleep(32);
   }
   tc_epi_sync();
-  float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
-  for (int j = b - 1; j >= jlo; --j) {
-    const size_t jidx = (size_t)j * a.Hpad + unit;
-    const float Aj = ld_cg(&a.aggA[jidx]), Bj = ld_cg(&a.aggB[jidx]);
-    Bacc = Aacc * Bj + Bacc;
-    Aacc = Aacc * Aj;
+  // All kLB aggregates (and the anchor) are loaded at once -- constant
+  // register indices, identity maps (A = 1, B = 0) past jlo -- and composed
+  // afterwards in the fixed order j = b-1 .. jlo (one L2 round trip instead
+  // of kLB dependent ones).  The identity steps leave the composed map
+  // bitwise unchanged (x*1 and fma(x, 0, y) are exact).  The barrier above
+  // orders these plain L2 loads after warp 0's acquires (and the compiler
+  // cannot hoist them across it).
+  float Aj[kLB], Bj[kLB];
+#pragma unroll
+  for (int k = 0; k < kLB; ++k) {
+    const int j = b - 1 - k;
+    const bool v = j >= jlo;
+    const size_t jidx = (size_t)(v ? j : 0) * a.Hpad + unit;
+    Aj[k] = v ? __ldcg(&a.aggA[jidx]) : 1.f;
+    Bj[k] = v ? __ldcg(&a.aggB[jidx]) : 0.f;
   }
-  const float anchor = jlo > 0 ? ld_cg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit])
+  const float anchor = jlo > 0 ? __ldcg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit])
                                 : (a.c_in != nullptr && unit < a.H ? a.c_in[unit] : 0.f);
+  float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
+#pragma unroll
+  for (int k = 0; k < kLB; ++k) {
+    Bacc = Aacc * Bj[k] + Bacc;
+    Aacc = Aacc * Aj[k];
+  }
   const float cin = Aacc * anchor + Bacc;
   a.incl[sidx] = Ablk * cin + Bblk;
   tc_epi_sync();
-  if (et == 0) {
-    __threadfence();
-    st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
-  }
+  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
   return cin;
 }
 
@@ -323,7 +423,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int t0 = b * a.T_b;
         for (int kt = 0; kt < a.nK; ++kt, ++it) {
           const int s = it % C::STAGES;
-          mbar_wait_sleep(&empty[s], ((it / C::STAGES) & 1) ^ 1);
+          // plain try_wait (the instruction suspends in hardware): a
+          // nanosleep back-off here overshot the stage release by up to ~1 us
+          // with each stage's MMAs taking ~0.3 us, starving the ring
+          mbar_wait(&empty[s], ((it / C::STAGES) & 1) ^ 1);
           unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
           if (a.dbg & 128) {  // timing experiment: no loads (MMAs read stale tiles)
             mbar_arrive(&full[s]);
@@ -344,9 +447,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer (one lane) ----------------
-    if (lane == 0) {
+    // ---------------- MMA issuer: the whole warp, one elected lane issues ----------------
+    {
       constexpr uint32_t idesc = tc_idesc<MODE>(128, N);
+      static_assert(C::A_BYTES == 16384 && C::KT / C::UK == 4 && (C::UK * C::ES) == 32,
+                    "tc_issue_ktile hard-codes 16 KB gate tiles and 4 K-steps of 32 B");
+      constexpr int HALF = 3 * C::A_BYTES + C::B_BYTES;  // hi -> lo plane offset (3xTF32)
       uint32_t it = 0, acc_it = 0;
       for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
         int ab = acc_it % C::NACC;
@@ -367,34 +473,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait(&full[s], (it / C::STAGES) & 1);
           tc_fence_after();
           unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
-          const uint64_t bdesc0 = sw128_desc(st + 3 * C::A_BYTES);
-          constexpr int HALF = 3 * C::A_BYTES + C::B_BYTES;
-#pragma unroll
-          for (int g = 0; g < ((a.dbg & 64) ? 0 : 3); ++g) {  // dbg 64 (timing): no MMAs
-            const uint64_t adesc0 = sw128_desc(st + g * C::A_BYTES);
-#pragma unroll
-            for (int kk = 0; kk < C::KT / C::UK; ++kk) {
-              // advance the start address along K inside the 128-B swizzle row
-              const uint64_t koff = (uint64_t)((kk * C::UK * C::ES) >> 4);
-              if (C::SPLIT == 2) {
-                const uint64_t blo = sw128_desc(st + HALF + 3 * C::A_BYTES) + koff;
-                const uint64_t alo = sw128_desc(st + HALF + g * C::A_BYTES) + koff;
-                tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kc | kk) != 0);
-                tc_mma<MODE>(dbase + g * N, adesc0 + koff, blo, idesc, 1);
-                tc_mma<MODE>(dbase + g * N, alo, bdesc0 + koff, idesc, 1);
-              } else {
-                tc_mma<MODE>(dbase + g * N, adesc0 + koff, bdesc0 + koff, idesc, (kt | kk) != 0);
-              }
-            }
-          }
-          tc_commit(&empty[s]);  // frees the smem stage once these MMAs have read it
+          if (!(a.dbg & 64))  // dbg 64 (timing): no MMAs
+            tc_issue_ktile<MODE>(dbase, sw128_desc(st), sw128_desc(st + 3 * C::A_BYTES), idesc, kc != 0, N,
+                                 (uint64_t)(HALF >> 4));
+          tc_commit_elect(&empty[s]);  // frees the smem stage once these MMAs have read it
           if (C::CHUNKED && (kc == C::CK - 1 || kt == a.nK - 1)) {
-            tc_commit(&acc_full[ab]);  // this K-chunk's partial products complete
+            tc_commit_elect(&acc_full[ab]);  // this K-chunk's partial products complete
             ++acc_it;
           }
         }
         if (!C::CHUNKED) {
-          tc_commit(&acc_full[ab]);  // accumulators of this item complete
+          tc_commit_elect(&acc_full[ab]);  // accumulators of this item complete
           ++acc_it;
         }
       }
@@ -497,23 +586,31 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             rf[j] = tc_sigmoid(rf[j]);
             ro[j] = tc_sigmoid(ro[j]);
           }
-          if (j < l) {
-            Bblk = rf[j] * Bblk + (1.f - rf[j]) * rz[j];
-            Ablk = rf[j] * Ablk;
-          }
+          // steps past the block end are identity steps (f = 1, z = 0): branch-free
+          if (j >= l) rf[j] = 1.f, rz[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          Bblk = rf[j] * Bblk + (1.f - rf[j]) * rz[j];
+          Ablk = rf[j] * Ablk;
         }
         const float cin = tc_lookback(a, b, u, unit, et, Ablk, Bblk);
         float c = cin;
+        const bool live = unit < a.H;
 #pragma unroll
-        for (int j = 0; j < N; ++j) {
-          if (j < l && unit < a.H) {
-            c = rf[j] * c + (1.f - rf[j]) * rz[j];
-            float h = ro[j] * tc_tanh(c);
+        for (int j = 0; j < N; ++j) {  // the c chain alone (one FMA per step) ...
+          c = rf[j] * c + (1.f - rf[j]) * rz[j];
+          rz[j] = c;
+        }
+#pragma unroll
+        for (int j = 0; j < N; ++j) {  // ... then the independent outputs
+          float h = ro[j] * tc_tanh(rz[j]);
+          if (j < l && live) {
             if (CELL == SRU) h = h + (1.f - ro[j]) * a.Xhw[(t0 + j) * a.ldhw + unit];
             store_h(a, (t0 + j) * a.ldh + unit, h);
           }
         }
-        if (b == a.nB - 1 && a.c_out != nullptr && unit < a.H) a.c_out[unit] = c;  // c_T of the sequence
+        if (b == a.nB - 1 && a.c_out != nullptr && live) a.c_out[unit] = c;  // c_T of the sequence
         continue;
       }
       const int ab = acc_it % C::NACC;
@@ -521,14 +618,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc_fence_after();
       const uint32_t tb = tmem + ab * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
       // (A) activations + block aggregate
+      // Branch-free per 16 columns: the three loads share one wait, the 48
+      // activations are independent (ILP for the one epilogue warp per
+      // scheduler), steps past the block end become identity steps (f = 1,
+      // z = 0: the aggregate and, in phase C, c are left exactly unchanged).
       for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
         float pz[16], pf[16], po[16];
-        tmem_ld16(tb + 0 * N + c0, pz);
-        tmem_ld16(tb + 1 * N + c0, pf);
-        tmem_ld16(tb + 2 * N + c0, po);
+        tmem_ld_gates16(tb + 0 * N + c0, tb + 1 * N + c0, tb + 2 * N + c0, pz, pf, po);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          if (CELL == SRU) {
+          if (a.dbg & 1024) {  // timing experiment: no activation math
+          } else if (CELL == SRU) {
             pf[j] = tc_sigmoid(pf[j] + bf);
             po[j] = tc_sigmoid(po[j] + br);
           } else {
@@ -536,17 +636,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             pf[j] = tc_sigmoid(pf[j]);
             po[j] = tc_sigmoid(po[j]);
           }
-          if (c0 + j < l) {
-            Bblk = pf[j] * Bblk + (1.f - pf[j]) * pz[j];
-            Ablk = pf[j] * Ablk;
-          }
+          if (c0 + j >= l) pf[j] = 1.f, pz[j] = 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          Bblk = pf[j] * Bblk + (1.f - pf[j]) * pz[j];
+          Ablk = pf[j] * Ablk;
         }
         tmem_st16(tb + 0 * N + c0, pz);
         tmem_st16(tb + 1 * N + c0, pf);
         tmem_st16(tb + 2 * N + c0, po);
       }
       tmem_st_wait();
-      const float cin = tc_lookback(a, b, u, unit, et, Ablk, Bblk);
+      const float cin = (a.dbg & 16) ? 0.f : tc_lookback(a, b, u, unit, et, Ablk, Bblk);  // 16: no look-back (timing)
       // (C) sequential recurrence from c_in and the output mix
       // row pointers advanced by a stride per step (no 64-bit index
       // arithmetic per store); the uniform peer / operand-copy tests hoisted
@@ -559,30 +661,47 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       unsigned char* op = a.Hop ? static_cast<unsigned char*>(a.Hop) +
                                       (t0 * ldop + unit) * (MODE == TC_BF16 ? 2 : 4)
                                 : nullptr;
-      for (int c0 = 0; c0 < N && c0 < l; c0 += 16) {
-        float z[16], f[16], o[16];
-        tmem_ld16(tb + 0 * N + c0, z);
-        tmem_ld16(tb + 1 * N + c0, f);
-        tmem_ld16(tb + 2 * N + c0, o);
+      for (int c0 = 0; c0 < N && c0 < l && !(a.dbg & 512); c0 += 16) {  // 512: no scan / stores (timing)
+        float z[16], f[16], o[16], xh[16];
+        if (CELL == SRU) {  // highway inputs first: their latency overlaps the TMEM loads and the chain
+#pragma unroll
+          for (int j = 0; j < 16; ++j) xh[j] = (c0 + j < l && live) ? xp[(int64_t)(c0 + j) * ldhw] : 0.f;
+        }
+        tmem_ld_gates16(tb + 0 * N + c0, tb + 1 * N + c0, tb + 2 * N + c0, z, f, o);
+        // the c chain alone (one FMA per step; f = 1, z = 0 past the block end) ...
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int col = c0 + j;
-          if (col < l && live) {
-            c = f[j] * c + (1.f - f[j]) * z[j];
-            float h = o[j] * tc_tanh(c);
-            if (CELL == SRU) h = h + (1.f - o[j]) * xp[(int64_t)col * ldhw];
-            hp[(int64_t)col * ldh] = h;
-            if (npeer > 0) {
+          c = f[j] * c + (1.f - f[j]) * z[j];
+          z[j] = c;
+        }
+        // ... then 16 independent outputs
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float h = o[j] * tc_tanh(z[j]);
+          if (CELL == SRU) h = h + (1.f - o[j]) * xh[j];
+          f[j] = h;
+        }
+        if (npeer == 0 && op == nullptr) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (c0 + j < l && live) hp[(int64_t)(c0 + j) * ldh] = f[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const int col = c0 + j;
+            if (col < l && live) {
+              const float h = f[j];
+              hp[(int64_t)col * ldh] = h;
               const int64_t i = (t0 + col) * ldh + unit;
 #pragma unroll
               for (int p = 0; p < kMaxPeers; ++p)
                 if (p < npeer) a.Hpeer[p][i] = h;
-            }
-            if (op != nullptr) {
-              if (MODE == TC_BF16)
-                reinterpret_cast<__nv_bfloat16*>(op)[(int64_t)col * ldop] = __float2bfloat16_rn(h);
-              else
-                reinterpret_cast<float*>(op)[(int64_t)col * ldop] = round_x(h, XR_TF32);
+              if (op != nullptr) {
+                if (MODE == TC_BF16)
+                  reinterpret_cast<__nv_bfloat16*>(op)[(int64_t)col * ldop] = __float2bfloat16_rn(h);
+                else
+                  reinterpret_cast<float*>(op)[(int64_t)col * ldop] = round_x(h, XR_TF32);
+              }
             }
           }
         }
