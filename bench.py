@@ -114,73 +114,124 @@ class ClockSampler:
 # our arm
 
 
-def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc=None):
-    """Dominant kernel = the fused layer kernel (one launch per layer).  The
-    pipe follows the kernel that actually ran (`tc`: the tcgen05 kernel ran
-    every layer); tensor-core modes that fell back to the FFMA kernel are
-    rated against the CUDA-core peak."""
+def _json(name):
+    p = os.path.join(REPO, "profiles", name)
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
+def ffma_peak():
+    d = _json("ffma_peak.json")
+    if d:
+        return d["fma_peak_tflops"], ("measured: tools/ffma_peak2.cu packed FFMA2, 32 independent chains, "
+                                      "profiles/ffma_peak.json (0.96 of nominal)")
+    return 148 * 128 * 2 * 1965e6 / 1e12, "nominal: 148 SMs x 128 lanes x 2 FLOP x 1965 MHz"
+
+
+def mma_floor_cycles(kind="f16"):
+    """Cycles per tcgen05.mma (M=128, one K-step, both operands in shared
+    memory) measured by tools/mma_rate.cu (profiles/mma_rate_r2.json): a
+    floor of ~51 cycles for any N <= 64, N/2 cycles above (math-bound)."""
+    d = _json("mma_rate_r2.json")
+    if d:
+        cg = 10 if kind == "tf32" else 1
+        rows = [r for r in d["rows"] if r["cta_group"] == cg and r["M"] == 128 and r["N"] <= 64]
+        if rows:
+            return max(r["cycles_per_mma"] for r in rows), "measured: tools/mma_rate.cu, profiles/mma_rate_r2.json"
+    return 51.3, "tools/mma_rate.cu round-2 measurement (51.3 cycles)"
+
+
+def tc_pick_n(T):
+    return 16 if T <= 16 else 32 if T <= 32 else 64 if T <= 64 else 128
+
+
+def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc=None, sm_mhz=None, nt=None):
+    """Roofline of the dominant kernel, per regime:
+
+    * tcgen05 path (bf16 / tf32 / fp32-accurate 3xTF32): the weights are
+      streamed into the tensor pipe once per block, so the applicable bound
+      is the slower of (a) the MMA instruction floor -- every 128 x N x K-step
+      MMA takes max(51 cycles, N/2) (tools/mma_rate.cu): below N = 128 the
+      pipe runs at N/102 of its peak -- and (b) the L2 -> shared-memory feed
+      of the weight and x tiles (measured 23.9 TB/s, tools/l2_tma_peak.cu).
+      `peak` is the algorithmic TFLOP/s that bound allows at this T_b;
+      the nominal tensor peak (MEASURED_PEAKS.json bf16) is reported beside.
+    * FFMA path (fp32 / f64 on CUDA cores): the FMA pipe (measured FFMA2 peak).
+    The reference's cold-cache byte model (traffic.py:26-27) is reported as
+    bytes only -- it describes the CPU, not these kernels."""
     if tc is None:
         tc = mode in ("bf16", "tf32", "f32x3")
     L = w.seq_len
     flops = workloads.flops_per_step(w) * L / launches_per_step
-    s_w = {"f32": 4, "tf32": 4, "bf16": 2, "f64": 8, "f32x3": 8}[mode]
+    sec = ms_per_launch / 1e3
+    mhz = sm_mhz or pk.get("sm_max_mhz", 1965.0)
+    achieved = flops / sec / 1e12
+    s_w = {"f32": 4, "tf32": 4, "bf16": 2, "f64": 8, "f32x3": 8, "f32_ffma": 4}[mode]
     s_a = 8 if mode == "f64" else 4
     params = workloads.param_count(w)
-    nblocks = -(-L // T_b)
-    # cold-cache traffic model (rnnblock traffic.py:26-27,64-68) + input/output once
-    bytes_model = (params * s_w * nblocks + (w.X.shape[1] + w.layers[-1].d_h) * s_a * L) / launches_per_step
-    sec = ms_per_launch / 1e3
-    mhz = pk.get("sm_max_mhz", 1965.0)
-    if not tc:
-        # CUDA-core pipe: MEASURED_PEAKS.json has no CUDA-core figure, so use the
-        # FFMA throughput measured on this pool by tools/ffma_peak.cu
-        fp = os.path.join(REPO, "profiles", "ffma_peak.json")
-        if os.path.exists(fp):
-            with open(fp) as f:
-                peak = json.load(f)["fma_peak_tflops"]
-            src = ("measured: tools/ffma_peak2.cu packed FFMA2, 32 independent chains, profiles/ffma_peak.json "
-                   "(0.96 of nominal)")
-        else:
-            peak = 148 * 128 * 2 * mhz * 1e6 / 1e12
-            src = f"nominal: 148 SMs x 128 lanes x 2 FLOP x {mhz:.0f} MHz"
-        if mode == "f64":
-            peak *= 0.5
-            src += " x 0.5 (fp64 rate)"
-        pipe = "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)"
-    else:
-        peak = pk["bf16_tflops"] * (0.5 if mode in ("tf32", "f32x3") else 1.0)
-        pipe = "tcgen05 " + mode
-        src = "MEASURED_PEAKS.json bf16_tflops" + (" x 0.5 (tf32 rate)" if mode in ("tf32", "f32x3") else "")
-        if mode == "f32x3":
-            src += "; algorithmic FLOPs only (3 tf32 products per fp32 product executed)"
-    achieved = flops / sec / 1e12
-    hbm = pk["hbm_gbs"]
-    # weight-stream roofline: the tensor-core kernel fetches every weight tile
-    # from L2 once per block (the same bytes as the cold-cache model); rated
-    # against the L2 read throughput measured by tools/l2_peak.cu
-    l2 = None
-    lp = os.path.join(REPO, "profiles", "l2_peak.json")
-    if os.path.exists(lp):
-        with open(lp) as f:
-            l2 = json.load(f)["l2_read_gbs"]
-    return {
-        "bound": "tensor" if tc else "compute",
-        "pipe": pipe,
-        "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-        "frac": round(achieved / peak, 4), "peak_source": src,
-        "traffic": traffic,
-        "flops_per_launch": flops, "ms_per_launch": round(ms_per_launch, 5),
-        "hbm_model": {
-            "note": "reference cold-cache byte model (weights re-fetched every block); "
-                    "the kernel keeps the weight slice SMEM/L2-resident, so this exceeds real DRAM traffic",
-            "bytes_per_launch": bytes_model, "achieved_gbs": round(bytes_model / sec / 1e9, 1),
-            "peak_gbs": hbm, "frac": round(bytes_model / sec / 1e9 / hbm, 4)},
-        "l2_model": None if l2 is None else {
-            "note": "same bytes against the measured L2 read throughput (profiles/l2_peak.json): the bound of "
-                    "the tensor-core kernel, which streams each weight tile from L2 once per block",
-            "achieved_gbs": round(bytes_model / sec / 1e9, 1), "peak_gbs": l2,
-            "frac": round(bytes_model / sec / 1e9 / l2, 4)},
-    }
+    cold = (params * s_w * -(-L // T_b) + (w.X.shape[1] + w.layers[-1].d_h) * s_a * L) / launches_per_step
+    out = {"traffic": traffic, "flops_per_launch": flops, "ms_per_launch": round(ms_per_launch, 5),
+           "reference_cold_cache_bytes_per_launch": cold}
+    if tc:
+        x3 = mode in ("f32", "f32x3")
+        T_eff = min(T_b, 32) if x3 else T_b  # 3xTF32 runs blocks of at most 32 steps
+        N = tc_pick_n(T_eff)
+        KT, es, kstep = (64, 2, 16) if mode == "bf16" else (32, 4, 8)
+        planes = 2 if x3 else 1
+        floor_cyc, floor_src = mma_floor_cycles("f16" if mode == "bf16" else "tf32")
+        cyc = max(floor_cyc, N / 2)
+        n_instr = 0.0
+        l2_bytes = 0.0
+        taps = 2 if w.kind.value == "qrnn" else 1
+        for lay in w.layers + (w.layers_bwd if w.bidirectional else []):
+            nU = -(-lay.d_h // 128)
+            nK = taps * -(-lay.d_in // KT)
+            nB = -(-L // T_eff)
+            n_instr += nU * nB * nK * 3 * (KT // kstep) * (3 if x3 else 1)
+            l2_bytes += nU * nB * nK * planes * (3 * 128 + N) * KT * es
+        n_instr /= launches_per_step
+        l2_bytes /= launches_per_step
+        t_mma = n_instr * cyc / 148 / (mhz * 1e6)
+        l2 = (_json("l2_peak.json") or {}).get("l2_read_gbs", 23887.0)
+        t_l2 = l2_bytes / (l2 * 1e9)
+        t_bound = max(t_mma, t_l2)
+        nominal = pk["bf16_tflops"] * (1.0 if mode == "bf16" else 0.5)
+        out.update({
+            "bound": "tensor", "pipe": "tcgen05 " + ("3xTF32 (fp32-accurate)" if x3 else mode),
+            "achieved": round(achieved, 3), "peak": round(flops / t_bound / 1e12, 2), "unit": "TFLOP/s",
+            "frac": round(t_bound / sec, 4),
+            "peak_source": (f"tcgen05 weight stream at N={N}: max(MMA issue floor {cyc:.1f} cycles x "
+                            f"{n_instr:.3g} MMAs / 148 SMs at {mhz:.0f} MHz = {t_mma * 1e6:.1f} us, "
+                            f"L2->SMEM tiles {l2_bytes / 1e9:.3g} GB / {l2:.0f} GB/s = {t_l2 * 1e6:.1f} us); "
+                            + floor_src),
+            "tensor_issue": {"mma_instructions": n_instr, "cycles_per_mma": cyc, "floor_us": round(t_mma * 1e6, 2),
+                             "frac": round(t_mma / sec, 4)},
+            "l2_feed": {"bytes": l2_bytes, "peak_gbs": l2, "achieved_gbs": round(l2_bytes / sec / 1e9, 1),
+                        "frac": round(t_l2 / sec, 4)},
+            "tensor_nominal": {"peak_tflops": nominal, "frac": round(achieved * (3 if x3 else 1) / nominal, 4),
+                               "note": "issued MMA work (3 products per fp32 product for 3xTF32) vs MEASURED_PEAKS "
+                                       "bf16 (x0.5 for tf32): reachable only with N >= 128, i.e. T_b >= 128"},
+        })
+        return out
+    peak, src = ffma_peak()
+    if mode == "f64":
+        peak *= 0.5
+        src += " x 0.5 (fp64 rate)"
+    out.update({"bound": "compute", "pipe": "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)",
+                "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4), "peak_source": src})
+    sw = _json("ncu_sweep_r1.json")
+    if sw and w.name == "cfg2" and mode in ("f32", "f32_ffma"):
+        for r in sw["rows"]:
+            if r["mode"] == "f32" and r["T_b"] == T_b:
+                cycles = r["us"] * 1e-6 * mhz * 1e6 * 148
+                out["smem_pipe"] = {
+                    "frac": round(r["smem_wavefronts_M"] * 1e6 / cycles, 4),
+                    "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared / SM cycles, profiles/ncu_sweep_r1.json "
+                              "(cfg2 f32, same kernel): the shared-memory pipe that feeds the resident weights"}
+    return out
 
 
 def load_traffic(workload, T_b, mode):
@@ -247,9 +298,83 @@ def kernel_name(r):
         return "ffma_reg (weights in registers, FFMA2, epilogue warp)"
     if all(r["tcgen05"]):
         return "tc_layer (tcgen05 + TMEM + TMA, look-back carry)"
+    if any(r["tcgen05"]):
+        return "mixed (tc_layer / ffma)"
     if all(r["ffma_ws"]):
         return "ffma_ws (TMA producer + mbarrier ring + epilogue warps)"
     return "ffma_layer"
+
+
+CONFIG_LINES = (("cfg1", "f32", (1, 4, 16)), ("cfg3", "f32", (1, 8, 32)), ("cfg3", "bf16", (1, 8, 32)),
+                ("cfg3", "tf32", (8, 32)), ("cfg4", "f32", (32,)), ("cfg4", "bf16", (32,)),
+                ("cfg5", "bf16", (16, 64)))
+
+
+def time_configs(args, local_rank, pk, mhz):
+    """Every other BASELINE config on this GPU (whole-model forwards: cfg3 =
+    projection + 6 SRU + logits, cfg5 = the fused sharded bidirectional
+    stack at G = 1), L2 flushed before every timed step; kernel recorded."""
+    import torch
+    import paper_1803_11389_b200 as P
+    from paper_1803_11389_b200 import p2p
+    from paper_1803_11389_b200.acoustic import AcousticSRU
+    dev = torch.device("cuda", local_rank)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    steps = max(3, min(args.steps, 10))
+    out = {}
+    cache = {}
+    for name, mode, blocks in CONFIG_LINES:
+        if name not in cache:
+            cache.clear()
+            cache[name] = workloads.make(name)
+        w = cache[name]
+        L = w.seq_len
+        X = torch.from_numpy(w.X).to(dev)
+        if name == "cfg3":
+            obj = AcousticSRU(w.proj, w.layers, w.logits, mode=mode, device=local_rank)
+            run = lambda T: obj.forward(X, T)  # noqa: E731
+            stack = obj.stack
+        elif name == "cfg5":
+            obj = p2p.P2PBidirSRU(w.layers, w.layers_bwd, 0, 1, blocks[0], mode, L, device=local_rank)
+            obj.connect_local([obj])
+
+            def run(T, obj=obj):
+                obj.block_size = T
+                return obj.forward(X)
+            stack = obj.stages[0][0]
+        else:
+            obj = P.DeviceStack(w.kind, w.layers, mode=mode, device=local_rank)
+            run = lambda T: obj.forward(X, T)  # noqa: E731
+            stack = obj
+        rows = {}
+        for T in blocks:
+            for _ in range(3):
+                run(T)
+            torch.cuda.synchronize()
+            tc = [bool(stack.query(9, li)) for li in range(stack.n_layers)]
+            reg = [bool(stack.query(10, li)) for li in range(stack.n_layers)]
+            wsk = [bool(stack.query(6, li)) for li in range(stack.n_layers)]
+            wst = [bool(stack.query(11, li)) for li in range(stack.n_layers)]
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+            for i in range(steps):
+                flush.fill_(float(i))
+                ev[i][0].record()
+                run(T)
+                ev[i][1].record()
+            torch.cuda.synchronize()
+            ms = sum(a.elapsed_time(b) for a, b in ev) / steps
+            rf = roofline_for(w, T, mode, ms, 1, pk, None, tc=all(tc), sm_mhz=mhz)
+            kern = ("tc_layer (tcgen05)" if all(tc) else "ffma_reg (register-resident)" if all(reg)
+                    else "ffma_ws weight-streaming" if all(wst) else "ffma_ws (SMEM-resident)" if all(wsk)
+                    else "ffma_layer")
+            rows[str(T)] = {"steps_per_s": round(L / (ms / 1e3), 1), "ms_per_step": round(ms, 4),
+                            "tflops": rf["achieved"], "frac": rf["frac"], "bound": rf["bound"],
+                            "peak_tflops": rf["peak"], "kernel": kern}
+        out[f"{name}/{mode}"] = {"seq_len": L, "blocks": rows}
+        obj.close()
+        del obj, X
+        torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args, rank, world, local_rank):
@@ -273,14 +398,19 @@ def run_ours(args, rank, world, local_rank):
     out = torch.empty((L, st.d_h[-1]), dtype=dt, device=dev)
     results = time_sweep(st, X, out, blocks, args, rank, world, local_rank, flush, clocks_for=args.block)
 
-    # the same workload in the tensor-core numerics modes (reported beside, not the headline)
+    # the same workload in the other numerics modes (reported beside, not the
+    # headline); "f32_ffma" = fp32 mode held on the FFMA kernels at every T_b
     extra = {}
     for m in [m for m in args.extra_modes.split(",") if m and m != args.mode]:
-        sm = P.DeviceStack(w.kind, w.layers, mode=m, device=local_rank)
+        real = "f32" if m == "f32_ffma" else m
+        if m == "f32_ffma":
+            os.environ["RNNB_F32_TC"] = "0"
+        sm = P.DeviceStack(w.kind, w.layers, mode=real, device=local_rank)
         outm = torch.empty((L, sm.d_h[-1]), dtype=sm.dtype, device=dev)
         Xm = X if sm.dtype == dt else X.to(sm.dtype)
         extra[m] = time_sweep(sm, Xm, outm, blocks, args, rank, world, local_rank, flush)
         sm.close()
+        os.environ.pop("RNNB_F32_TC", None)
 
     # end-to-end through the public C-ABI host entry point (pinned host buffers)
     dist = world > 1
@@ -313,27 +443,42 @@ def run_ours(args, rank, world, local_rank):
            "timing": f"wall clock per call, median of {e_steps}",
            "api": "rnnb_forward_host (C ABI, pinned host X/H)"}
 
+    # the partitioned BASELINE configs across all ranks (cfg4 layer pipeline,
+    # cfg5 hidden sharding): strong scaling; at N = 1 these are the anchors
+    partitioned = {}
+    if args.partitioned:
+        for part, wl in (("pipeline", "cfg4"), ("hidden", "cfg5")):
+            blk = 32 if part == "pipeline" else 64
+            partitioned[part] = run_partitioned(args, rank, world, local_rank, workload=wl, partition=part,
+                                                mode="bf16", block=blk, chunk=args.chunk)
     if rank != 0:
         st.close()
         return None
     pk, pk_src = peaks()
 
+    head = results[args.block]
+    mhz = (head["clocks"] or {}).get("sm_mhz")
+
     def sweep_of(res, mode):
         out_ = {}
         for T_b, r in res.items():
             rf = roofline_for(w, T_b, mode, r["ms_per_step"] / (r["launches"] or 1), r["launches"] or 1,
-                              pk, None, tc=all(r["tcgen05"]))
-            out_[str(T_b)] = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
-                              "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"],
-                              "tflops": rf["achieved"], "pipe": rf["pipe"], "kernel": kernel_name(r),
-                              "hbm_model_frac": rf["hbm_model"]["frac"],
-                              "l2_model_frac": rf["l2_model"]["frac"] if rf["l2_model"] else None}
+                              pk, None, tc=all(r["tcgen05"]), sm_mhz=mhz)
+            row = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
+                   "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"], "bound": rf["bound"],
+                   "tflops": rf["achieved"], "peak_tflops": rf["peak"], "pipe": rf["pipe"],
+                   "kernel": kernel_name(r)}
+            if "smem_pipe" in rf:
+                row["smem_pipe_frac"] = rf["smem_pipe"]["frac"]
+            if rf["bound"] == "tensor":
+                row["tensor_issue_frac"] = rf["tensor_issue"]["frac"]
+                row["l2_feed_frac"] = rf["l2_feed"]["frac"]
+            out_[str(T_b)] = row
         return out_
 
-    head = results[args.block]
     roof = roofline_for(w, args.block, args.mode, head["ms_per_step"] / (head["launches"] or 1),
                         head["launches"] or 1, pk, load_traffic(args.workload, args.block, args.mode),
-                        tc=all(head["tcgen05"]))
+                        tc=all(head["tcgen05"]), sm_mhz=mhz)
     roof["peaks_file"] = pk_src
     resident = [bool(st.query(3, li)) for li in range(st.n_layers)]
     line = {
@@ -358,6 +503,10 @@ def run_ours(args, rank, world, local_rank):
         "modes": {m: sweep_of(r, m) for m, r in extra.items()},
         "clocks": head["clocks"],
     }
+    if partitioned:
+        line["partitioned"] = partitioned
+    if args.configs and world == 1:
+        line["configs"] = time_configs(args, local_rank, pk, mhz)
     if args.cpu_baseline and world == 1:  # the CPU baseline is a rank-0, N=1 measurement
         line["cpu_baseline"] = cpu_baseline(args, w, sample_steps=args.cpu_sample)
     st.close()
@@ -368,7 +517,8 @@ def run_ours(args, rank, world, local_rank):
 # partitioned configs across ranks: the fused peer-memory partitions (p2p.py)
 
 
-def run_partitioned(args, rank, world, local_rank):
+def run_partitioned(args, rank, world, local_rank, workload=None, partition=None, mode=None, block=None,
+                    chunk=None):
     """BASELINE cfg4 (--partition pipeline: layer pipeline of time chunks) or
     cfg5 (--partition hidden: hidden-dimension sharding with the all-gather
     in the epilogue) over the ranks, one GPU each (CUDA IPC between the rank
@@ -381,6 +531,12 @@ def run_partitioned(args, rank, world, local_rank):
     from paper_1803_11389_b200 import p2p
     from paper_1803_11389_b200.partition import layer_ranges
 
+    import copy
+    args = copy.copy(args)
+    for k, v in (("workload", workload), ("partition", partition), ("mode", mode), ("block", block),
+                 ("chunk", chunk)):
+        if v is not None:
+            setattr(args, k, v)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     w = workloads.make(args.workload)
@@ -508,25 +664,51 @@ def _oracle():
     return O
 
 
-def cpu_baseline(args, w, sample_steps):
-    O = _oracle()
-    cores = os.cpu_count() or 1
-    O.set_threads(cores)
-    L = min(sample_steps, w.seq_len)
-    X = np.ascontiguousarray(w.X[:L])
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _time_oracle(O, w, X, T_b, seconds):
     layers = [lay.mats() for lay in w.layers]
-    O.run_blocked(w.kind.value, layers, X, args.block)  # warm-up
+    O.run_blocked(w.kind.value, layers, X, T_b)  # warm-up
     times = []
-    t_end = time.perf_counter() + args.cpu_seconds
+    t_end = time.perf_counter() + seconds
     while time.perf_counter() < t_end or len(times) < 3:
         t0 = time.perf_counter()
-        O.run_blocked(w.kind.value, layers, X, args.block)
+        O.run_blocked(w.kind.value, layers, X, T_b)
         times.append(time.perf_counter() - t0)
-    med = statistics.median(times)
+    return statistics.median(times), len(times)
+
+
+def cpu_baseline(args, w, sample_steps):
+    """The oracle's C port of rnnblock's fast path on this box's host cores
+    (all threads, plus a 1-thread row and the CPU
+    model), on a bounded prefix of the same workload."""
+    O = _oracle()
+    cores = os.cpu_count() or 1
+    L = min(sample_steps, w.seq_len)
+    X = np.ascontiguousarray(w.X[:L])
+    O.set_threads(cores)
+    med, n = _time_oracle(O, w, X, args.block, args.cpu_seconds)
+    L1 = max(args.block, L // 8)  # the 1-thread row on a shorter prefix (same per-step work)
+    O.set_threads(1)
+    med1, n1 = _time_oracle(O, w, np.ascontiguousarray(w.X[:L1]), args.block, min(args.cpu_seconds, 8.0))
+    O.set_threads(cores)
     return {"value": round(L / med, 1), "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{args.workload} first {L} of {w.seq_len} steps, T_b={args.block}, "
-                      f"median of {len(times)} runs, oracle/ C port of rnnblock fast kernel, "
-                      f"OpenMP {cores} threads"}
+                      f"median of {n} runs, oracle/ C port of rnnblock fast kernel, "
+                      f"OpenMP {cores} threads",
+            "single_thread": {"value": round(L1 / med1, 1), "unit": UNIT, "cores": 1,
+                              "sample": f"{args.workload} first {L1} steps, T_b={args.block}, median of {n1} runs"}}
 
 
 def run_reference(args, rank, world):
@@ -556,7 +738,8 @@ def run_reference(args, rank, world):
             "data": "synthetic (seeded PCG64, BASELINE.json distributions)",
             "config": {"workload": args.workload, "block_size": args.block, "mode": "f32",
                        "seq_len_sample": L},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -570,15 +753,19 @@ def main():
     ap.add_argument("--block", type=int, default=32)
     ap.add_argument("--mode", default="f32", choices=("f32", "f64", "bf16", "tf32"))
     ap.add_argument("--no-sweep", dest="sweep", action="store_false")
-    ap.add_argument("--extra-modes", default="bf16,tf32,f32x3",
-                    help="tensor-core numerics modes timed beside the headline mode")
+    ap.add_argument("--extra-modes", default="f32_ffma,bf16,tf32",
+                    help="numerics modes timed beside the headline mode (f32_ffma: fp32 on the FFMA kernels)")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--cpu-sample", type=int, default=512, help="time steps in the CPU sample")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--partition", choices=("replicas", "pipeline", "hidden"), default="replicas",
                     help="replicas: N independent copies of the workload (cfg1/cfg2 do not shard); "
                          "pipeline: cfg4 layer pipeline across ranks; hidden: cfg5 hidden sharding")
-    ap.add_argument("--chunk", type=int, default=4096, help="pipeline chunk (steps, a multiple of --block)")
+    ap.add_argument("--chunk", type=int, default=1024, help="pipeline chunk (steps, a multiple of --block)")
+    ap.add_argument("--no-partitioned", dest="partitioned", action="store_false",
+                    help="skip the cfg4 pipeline / cfg5 hidden-sharding sub-object")
+    ap.add_argument("--no-configs", dest="configs", action="store_false",
+                    help="skip the other BASELINE configs (single-GPU lines)")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warning: W < 3 warm-up steps violates the timing rules; using 3")

@@ -181,17 +181,25 @@ def cfg4(oracle):
     return w, mats, xp, ref, cref
 
 
-@pytest.mark.parametrize("mode", ["f32", "bf16", "f32x3"])
-def test_cfg4_all_layers_prefix(P, oracle, cfg4, mode):
+@pytest.mark.parametrize("mode", ["f32_ffma", "f32", "bf16", "f32x3"])
+def test_cfg4_all_layers_prefix(P, oracle, cfg4, mode, monkeypatch):
     """8 x QRNN-2048 on an 8192-step prefix, T_b=32: output and every
-    layer's c_T vs the fp32 oracle (fp32 bound for f32 and f32x3)."""
+    layer's c_T vs the fp32 oracle (fp32 bound for the fp32 modes: the
+    weight-streaming FFMA kernel, fp32 mode's default 3xTF32 tcgen05, f32x3)."""
     import torch
     w, mats, xp, ref, cref = cfg4
+    if mode == "f32_ffma":
+        monkeypatch.setenv("RNNB_F32_TC", "0")
+        mode = "f32"
+        ffma = True
+    else:
+        ffma = False
     st = P.DeviceStack("qrnn", w.layers, mode=mode)
     c = torch.zeros(8 * 2048, device="cuda")
     H = st.forward(_cuda(xp), 32, c_state=c).cpu().numpy()
-    if mode == "f32":
+    if ffma:
         assert all(st.query(11, li) == 1 for li in range(8)), "weight-streaming FFMA kernel did not run"
+        mode = "f32_ffma"
     else:
         assert all(st.query(9, li) == 1 for li in range(8)), "tcgen05 kernel did not run"
     cs = c.cpu().numpy().reshape(8, 2048)
@@ -234,13 +242,14 @@ def test_cfg4_bf16_per_layer_rounded_operands(P, oracle, cfg4):
 
 
 @pytest.mark.parametrize("mode", ["f32", "bf16"])
-def test_cfg4_full_sequence_window(P, oracle, cfg4, mode):
+def test_cfg4_full_sequence_window(P, oracle, cfg4, mode, monkeypatch):
     """The full 65536-step sequence (2048 blocks x 8 layers through the
     look-back / the streamed FFMA passes): one call == the same sequence in
     two calls split at L-1024 with carried (c, x_carry) (bitwise for the
     FFMA kernel, look-back re-anchored at the split for tcgen05), and the
     last 1024 steps == the oracle restarted from the GPU's state there."""
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", "0")  # f32 here = the FFMA kernels (bitwise split invariance)
     w, mats, _, _, _ = cfg4
     L = w.X.shape[0]
     s = L - WINDOW4

@@ -143,10 +143,14 @@ def test_baseline_cfg1_full(P, oracle):
         assert_f32(H, g["cfg1_T16_H"])
 
 
-def test_baseline_cfg2_full(P, oracle):
+@pytest.mark.parametrize("f32_tc", ["0", "1"])
+def test_baseline_cfg2_full(P, oracle, f32_tc, monkeypatch):
     """BASELINE cfg2 (QRNN 1024, L=2048) at full size: reference row
-    subsample + c_T, plus the oracle over the whole output at every T_b."""
+    subsample + c_T, plus the oracle over the whole output at every T_b --
+    on the FFMA kernels (RNNB_F32_TC=0) and on fp32 mode's default dispatch
+    (3xTF32 tcgen05 from T_b = 16)."""
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", f32_tc)
     from paper_1803_11389_b200 import workloads
     g = np.load(os.path.join(GOLDEN, "baseline_cfg.npz"))
     w = workloads.make("cfg2")
@@ -159,17 +163,22 @@ def test_baseline_cfg2_full(P, oracle):
         if T == 32:
             assert_f32(H[g["cfg2_T32_rows"]], g["cfg2_T32_Hrows"])
             assert_f32(c.cpu().numpy(), g["cfg2_T32_c"])
-        assert st.query(3) == 1 and st.query(6) == 1  # SMEM-resident, warp-specialised
+        if f32_tc == "0" or T < 16:
+            assert st.query(3) == 1 and st.query(6) == 1  # SMEM-resident, warp-specialised FFMA
+        else:
+            assert st.query(9) == 1  # 3xTF32 on tcgen05
         ref, cref, _ = oracle.run_blocked("qrnn", layers, w.X, T, return_state=True)
         assert_f32(H, ref)
         assert_f32(c.cpu().numpy(), cref[0])
     st.close()
 
 
-def test_streaming_state_carry_equals_whole_sequence(P, oracle):
+def test_streaming_state_carry_equals_whole_sequence(P, oracle, monkeypatch):
     """c and x_carry in/out across calls: two half-sequence calls on a block
-    boundary reproduce the whole-sequence call bit for bit."""
+    boundary reproduce the whole-sequence call bit for bit (FFMA kernels:
+    the per-unit dot products never depend on the chunking)."""
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", "0")
     for kind in ("sru", "qrnn"):
         layers = oracle.generate_layers(kind, 128, 128, 2, 21, np.float32)
         X = np.random.default_rng(3).standard_normal((256, 128)).astype(np.float32)
@@ -465,6 +474,7 @@ def test_wide_pass_kernels(P, oracle, kind, d, monkeypatch):
     at NT=16 and the opt-in NT=32 pass, including a remainder block and a
     partial last K chunk (d=520), vs the oracle."""
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", "0")
     layers = oracle.generate_layers(kind, d, d, 2, 61, np.float32)
     X = np.random.default_rng(15).standard_normal((301, d)).astype(np.float32)
     Xd = torch.from_numpy(X).cuda()
@@ -483,8 +493,10 @@ def test_host_streaming_matches_device(P, oracle, kind, d, L, T, monkeypatch):
     """rnnb_forward_host's streaming mode (one layer launch fed by the copy
     stream through a device row counter, chunks drained by a wait-value copy
     stream) and its chunked fallback are bitwise equal to the device call,
-    including carried c / x_carry in-out state."""
+    including carried c / x_carry in-out state (FFMA kernels; streaming
+    needs them)."""
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", "0")
     layers = oracle.generate_layers(kind, d, d, 1, 71, np.float32)
     X = np.random.default_rng(16).standard_normal((L, d)).astype(np.float32)
     st = P.DeviceStack(kind, layers)
@@ -515,6 +527,7 @@ def test_weight_streaming_kernel(P, oracle, kind, d, n_layers, monkeypatch):
     remainder block, carried state and an H not a multiple of 14, vs the
     oracle and vs the generic kernel (RNNB_WSTREAM=0)."""
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", "0")
     layers = oracle.generate_layers(kind, d, d, n_layers, 81, np.float32)
     L = 203
     X = np.random.default_rng(19).standard_normal((L, d)).astype(np.float32)

@@ -27,8 +27,9 @@ def pg():
     dist.destroy_process_group()
 
 
-def test_pipeline_stage_on_gpu_bitwise_equals_whole_sequence(pg, oracle):
+def test_pipeline_stage_on_gpu_bitwise_equals_whole_sequence(pg, oracle, monkeypatch):
     import torch
+    monkeypatch.setenv("RNNB_F32_TC", "0")  # f32: FFMA kernels, chunking-invariant bitwise
     import paper_1803_11389_b200 as P
     from paper_1803_11389_b200 import partition
     layers = oracle.generate_layers("qrnn", 256, 256, 4, 7, np.float32)

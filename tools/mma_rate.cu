@@ -121,6 +121,12 @@ __global__ void __launch_bounds__(128, 1) k_mma(int M, int N, int R, long long* 
           asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                            su32(&bar2))
                        : "memory");
+      } else if (MIMIC & 128) {  // kind::tf32 (K = 8 per MMA: 128 rows x 32 B of A, same bytes as bf16)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+            "l"(ad + koff), "l"(bd + koff), "r"((idesc & ~((7u << 7) | (7u << 10))) | (2u << 7) | (2u << 10)),
+            "r"(r));
       } else if (CG == 1)
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -180,6 +186,7 @@ int main(int argc, char** argv) {
   cudaFuncSetAttribute(k_mma<1, 7>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_mma<1, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_mma<1, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(k_mma<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_mma<1, 23>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_mma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   struct Shape { int cg, M, N; };
@@ -188,7 +195,9 @@ int main(int argc, char** argv) {
   // tile switch only, 5 = accumulator switch only, 6 = commits only
   // 7 / 8 = the full pattern with a commit every 24 / 48 MMAs
   // 9 = the full pattern issued as one asm block of 12 MMAs + commit per k-tile
-  const Shape shapes[] = {{9, 128, 64}, {9, 128, 32}, {9, 128, 16}, {3, 128, 64}, {4, 128, 64}, {5, 128, 64}, {6, 128, 64}, {7, 128, 64}, {8, 128, 64},
+  // 10 = kind::tf32 (flops counted at the bf16 K = 16 per MMA: halve for tf32)
+  const Shape shapes[] = {{9, 128, 64}, {9, 128, 32}, {9, 128, 16}, {10, 128, 16}, {10, 128, 32}, {10, 128, 64},
+                          {10, 128, 128}, {3, 128, 64}, {4, 128, 64}, {5, 128, 64}, {6, 128, 64}, {7, 128, 64}, {8, 128, 64},
                           {7, 128, 32}, {8, 128, 32}, {1, 128, 16}, {1, 128, 32}, {1, 128, 64}, {1, 128, 128}, {1, 128, 256}, {1, 64, 64},
                           {1, 64, 128}, {1, 64, 256}, {2, 256, 32}, {2, 256, 64}, {2, 256, 128}, {2, 256, 256}};
   printf("{\"R\": %d, \"sms\": %d, \"rows\": [\n", R, nsm);
@@ -217,6 +226,7 @@ int main(int argc, char** argv) {
                       : s.cg == 5 ? cudaLaunchKernelEx(&cfg, k_mma<1, 2>, s.M, s.N, R, dcyc)
                       : s.cg == 6 ? cudaLaunchKernelEx(&cfg, k_mma<1, 4>, s.M, s.N, R, dcyc)
                       : s.cg == 9 ? cudaLaunchKernelEx(&cfg, k_mma<1, 32>, s.M, s.N, R, dcyc)
+                      : s.cg == 10 ? cudaLaunchKernelEx(&cfg, k_mma<1, 128>, s.M, s.N, R, dcyc)
                       : s.cg == 7 ? cudaLaunchKernelEx(&cfg, k_mma<1, 15>, s.M, s.N, R, dcyc)
                       : s.cg == 8 ? cudaLaunchKernelEx(&cfg, k_mma<1, 23>, s.M, s.N, R, dcyc)
                                   : cudaLaunchKernelEx(&cfg, k_mma<2>, s.M, s.N, R, dcyc);
