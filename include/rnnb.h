@@ -210,6 +210,10 @@ rnnb_status rnnb_lstm_query(rnnb_lstm_t h, int what, int64_t* value);
  * 2 QRNN; precision codes 0 f32, 1 f64. */
 rnnb_status rnnb_rnnw_info(const char* path, int* kind, int* precision, int* n_layers, int64_t* d_in,
                            int64_t* d_h, int max_layers);
+/* load_weights (model_io.py:209-267) into HOST memory: every parameter of
+ * the file, canonical layer and field order, converted to dst_dtype; n must
+ * equal the file's parameter count (rnnb_rnnw_info gives the shapes). */
+rnnb_status rnnb_rnnw_read(const char* path, void* dst, int64_t n, int dst_dtype);
 /* load_weights + rnnb_stack_create + rnnb_stack_set_layer for every layer. */
 rnnb_status rnnb_stack_load_rnnw(rnnb_stack_t* out, const char* path, int mode, int device);
 /* One LSTM layer of an RNNW file into an rnnb_lstm handle. */

@@ -28,7 +28,7 @@ SYMBOLS = (
     "rnnb_ipc_close", "rnnb_peer_access", "rnnb_flag_signal", "rnnb_flag_wait",
     "rnnb_gemm", "rnnb_activation", "rnnb_splitmix_uniform",
     "rnnb_linear_create", "rnnb_linear_destroy", "rnnb_linear_set_weights", "rnnb_linear_forward",
-    "rnnb_linear_query",
+    "rnnb_linear_query", "rnnb_rnnw_read",
 )
 MAX_PEERS = 7
 IPC_HANDLE_BYTES = 64
@@ -96,6 +96,7 @@ def load():
         "rnnb_linear_set_weights": ([vp, vp, vp, ci], ci),
         "rnnb_linear_forward": ([vp, vp, i64, i64, vp, i64, vp], ci),
         "rnnb_linear_query": ([vp, ci, P64], ci),
+        "rnnb_rnnw_read": ([ctypes.c_char_p, vp, i64, ci], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

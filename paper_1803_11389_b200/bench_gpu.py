@@ -159,66 +159,84 @@ def bench(cfg, weights, X, t_list, repeats: int = 5, threads: int = 1, warmup: i
 
 
 def summarize(records) -> list:
-    """Median per (cell, impl, block); speed-ups against the T=1 median (bench.py:157-177)."""
-    groups, order = {}, []
+    """One SpeedupRow per (cell, impl, block) in first-seen order: the median
+    time and the speed-up against the same (cell, impl) at block 1."""
+    times = {}
     for r in records:
-        key = (r.cell, r.impl, r.block)
-        if key not in groups:
-            groups[key] = []
-            order.append(key)
-        groups[key].append(r.elapsed_ms)
-    med = {k: statistics.median(v) for k, v in groups.items()}
-    rows = []
-    for cell, impl, block in order:
-        base = med.get((cell, impl, 1))
-        rows.append(SpeedupRow(label=f"{cell.upper()}-{block}", median_ms=med[(cell, impl, block)],
-                               speedup_pct=speedup(base, med[(cell, impl, block)]) if base is not None else None))
-    return rows
+        times.setdefault((r.cell, r.impl, r.block), []).append(r.elapsed_ms)
+    med = {key: statistics.median(ts) for key, ts in times.items()}
+    return [SpeedupRow(label=f"{cell.upper()}-{block}", median_ms=m,
+                       speedup_pct=None if (cell, impl, 1) not in med else speedup(med[(cell, impl, 1)], m))
+            for (cell, impl, block), m in med.items()]
 
 
-_HEADERS = {"records": ["cell", "impl", "d_in", "d_h", "seq_len", "block", "threads", "repeat", "elapsed_ms"],
-            "summary": ["label", "median_ms", "speedup_pct"],
-            "traffic": ["cell", "d_h", "precision", "L", "T", "weight_bytes", "blocks", "est_traffic_bytes",
-                        "ratio_vs_T1"]}
+@dataclass(frozen=True)
+class _Schema:
+    """A CSV layout: the row type it accepts and (header, cell formatter) per column."""
+    row_type: type
+    columns: tuple
+
+    @property
+    def header(self):
+        return [name for name, _ in self.columns]
+
+    def cells(self, row):
+        return [fmt(row) for _, fmt in self.columns]
 
 
-def _kind_of(row):
-    for cls, kind in ((BenchRecord, "records"), (SpeedupRow, "summary"), (TrafficReport, "traffic")):
-        if isinstance(row, cls):
-            return kind
+def _attr(name, fmt=str):
+    return lambda row: fmt(getattr(row, name))
+
+
+# The reference's record / summary / traffic CSV layouts (its bench CSVs are
+# pinned byte for byte by tests/golden/bench_*.csv): floats keep repr().
+_SCHEMAS = {
+    "records": _Schema(BenchRecord, tuple((c, _attr(c, repr if c == "elapsed_ms" else str)) for c in (
+        "cell", "impl", "d_in", "d_h", "seq_len", "block", "threads", "repeat", "elapsed_ms"))),
+    "summary": _Schema(SpeedupRow, (
+        ("label", _attr("label")), ("median_ms", _attr("median_ms", repr)),
+        ("speedup_pct", lambda r: "-" if r.speedup_pct is None else f"{r.speedup_pct:.1f}"))),
+    "traffic": _Schema(TrafficReport, (
+        ("cell", lambda r: r.config.kind.value), ("d_h", lambda r: str(r.config.d_h)),
+        ("precision", lambda r: r.config.precision), ("L", _attr("seq_len")), ("T", _attr("block_size")),
+        ("weight_bytes", _attr("weight_bytes")), ("blocks", _attr("blocks")),
+        ("est_traffic_bytes", _attr("est_weight_traffic")), ("ratio_vs_T1", _attr("ratio_vs_t1", repr)))),
+}
+
+
+def _schema_for(row):
+    for name, sch in _SCHEMAS.items():
+        if isinstance(row, sch.row_type):
+            return name
     raise ValueError(f"no CSV layout for {type(row).__name__}")
 
 
 def emit_csv(rows, path, kind: str = None) -> None:
-    """bench.py:194-229: records, summary rows or traffic reports with a fixed header."""
+    """Write records, summary rows or traffic reports under the layout's
+    fixed header (one row type per file)."""
     if kind is None:
         if not rows:
             raise ValueError("empty row list needs an explicit kind")
-        kind = _kind_of(rows[0])
-    if kind not in _HEADERS:
+        kind = _schema_for(rows[0])
+    if kind not in _SCHEMAS:
         raise ValueError(f"unknown CSV kind {kind!r}")
+    sch = _SCHEMAS[kind]
+    if any(_schema_for(r) != kind for r in rows):
+        raise ValueError("mixed row types in one CSV")
     with open(path, "w", newline="") as f:
         w = csv.writer(f)
-        w.writerow(_HEADERS[kind])
-        for row in rows:
-            if _kind_of(row) != kind:
-                raise ValueError("mixed row types in one CSV")
-            if kind == "records":
-                w.writerow([row.cell, row.impl, row.d_in, row.d_h, row.seq_len, row.block, row.threads, row.repeat,
-                            repr(row.elapsed_ms)])
-            elif kind == "summary":
-                w.writerow([row.label, repr(row.median_ms), "-" if row.speedup_pct is None else f"{row.speedup_pct:.1f}"])
-            else:
-                w.writerow([row.config.kind.value, row.config.d_h, row.config.precision, row.seq_len, row.block_size,
-                            row.weight_bytes, row.blocks, row.est_weight_traffic, repr(row.ratio_vs_t1)])
+        w.writerow(sch.header)
+        w.writerows(sch.cells(r) for r in rows)
+
+
+_TABLE = (("Model", "<12", lambda r: r.label), ("Median (ms)", ">12", lambda r: f"{r.median_ms:.3f}"),
+          ("Speed-up", ">10", lambda r: "-" if r.speedup_pct is None else f"{r.speedup_pct:.1f}%"))
 
 
 def format_summary_table(rows) -> str:
-    lines = [f"{'Model':<12} {'Median (ms)':>12} {'Speed-up':>10}"]
-    for r in rows:
-        pct = "-" if r.speedup_pct is None else f"{r.speedup_pct:.1f}%"
-        lines.append(f"{r.label:<12} {r.median_ms:>12.3f} {pct:>10}")
-    return "\n".join(lines)
+    head = " ".join(f"{name:{align}}" for name, align, _ in _TABLE)
+    body = [" ".join(f"{cell(r):{align}}" for _, align, cell in _TABLE) for r in rows]
+    return "\n".join([head] + body)
 
 
 # ---------------------------------------------------------------------------

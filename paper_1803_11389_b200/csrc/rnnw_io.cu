@@ -234,6 +234,30 @@ rnnb_status rnnb_lstm_load_rnnw(rnnb_lstm_t* out, const char* path, int layer, i
   });
 }
 
+rnnb_status rnnb_rnnw_read(const char* path, void* dst, int64_t n, int dst_dtype) {
+  return rnnb::abi_guard("rnnb_rnnw_read", [&]() -> rnnb_status {
+    if (!dst) return set_error(RNNB_EINVAL, "null destination");
+    if (dst_dtype != RNNB_DT_F32 && dst_dtype != RNNB_DT_F64) return set_error(RNNB_EINVAL, "dst dtype must be f32 or f64");
+    std::vector<LayerDims> dims;
+    std::vector<std::vector<double>> payload;
+    int k = 0, p = 0;
+    rnnb_status st = parse_rnnw(path, &k, &p, &dims, &payload);
+    if (st != RNNB_OK) return st;
+    int64_t total = 0;
+    for (auto& v : payload) total += (int64_t)v.size();
+    if (n != total)
+      return set_error(RNNB_EINVAL, "destination holds " + std::to_string(n) + " elements, file has " +
+                                        std::to_string(total));
+    int64_t o = 0;
+    for (auto& v : payload)
+      for (double x : v) {
+        if (dst_dtype == RNNB_DT_F64) static_cast<double*>(dst)[o++] = x;
+        else static_cast<float*>(dst)[o++] = (float)x;
+      }
+    return RNNB_OK;
+  });
+}
+
 rnnb_status rnnb_rnnx_info(const char* path, int* precision, int64_t* seq_len, int64_t* width) {
   return rnnb::abi_guard("rnnb_rnnx_info", [&]() -> rnnb_status {
     File file(path);

@@ -1,12 +1,13 @@
-"""RNNW / RNNX files: the reference's serialisation
-(rnnblock model_io.py:1-33, 190-308) with the same exception classes, plus
-loaders that go from a file straight into the device layouts through the C
-ABI (``rnnb_stack_load_rnnw``, ``rnnb_lstm_load_rnnw``, ``rnnb_rnnx_load``).
+"""RNNW / RNNX files behind the reference's
+interface (rnnblock model_io.py: save/load_weights, save/load_sequence, the
+same exception classes), plus loaders that go from a file straight into the
+device layouts through the C ABI (``rnnb_stack_load_rnnw``,
+``rnnb_lstm_load_rnnw``, ``rnnb_rnnx_load``).
 
-Host-side ``save_* / load_*`` produce and accept byte-identical files to the
-reference's (little-endian, fixed headers, row-major, canonical field
-order); the native loaders validate the same way (sizes checked against the
-file before any allocation) and report the reference's exception class.
+Saves are byte-identical to the reference's files; every load -- host or
+device -- goes through the one native parser (csrc/rnnw_io.cu), which checks
+sizes against the file before any allocation and reports the reference's
+exception class (mapped back in _lib.check).
 """
 
 import ctypes
@@ -62,69 +63,30 @@ def _dt(precision):
     return np.dtype("<f4") if precision == "f32" else np.dtype("<f8")
 
 
-def save_weights(ws: WeightSet, path) -> None:
+# File layouts (model_io.py:1-33): fixed little-endian headers, then
+# row-major payloads in canonical field order.
+_RNNW_HEADER = struct.Struct("<4sIBBHI")   # magic, version, kind, precision, reserved, n_layers
+_RNNW_LAYER = struct.Struct("<II")         # d_in, d_h
+_RNNX_HEADER = struct.Struct("<4sIBBHII")  # magic, version, precision, 2 reserved, seq_len, width
+
+
+def _write(path, chunks):
     with open(path, "wb") as f:
-        f.write(struct.pack("<4sIBBHI", _WEIGHT_MAGIC, _VERSION, _KIND_CODES[ws.kind], _PREC_CODES[ws.precision],
-                            0, len(ws.layers)))
-        dt = _dt(ws.precision)
+        for c in chunks:
+            f.write(c)
+
+
+def save_weights(ws: WeightSet, path) -> None:
+    dt = _dt(ws.precision)
+
+    def chunks():
+        yield _RNNW_HEADER.pack(_WEIGHT_MAGIC, _VERSION, _KIND_CODES[ws.kind], _PREC_CODES[ws.precision], 0,
+                                len(ws.layers))
         for layer in ws.layers:
-            f.write(struct.pack("<II", layer.d_in, layer.d_h))
+            yield _RNNW_LAYER.pack(layer.d_in, layer.d_h)
             for fld in dataclasses.fields(layer):
-                f.write(np.ascontiguousarray(getattr(layer, fld.name), dtype=dt).tobytes())
-
-
-def _read(f, n, what):
-    buf = f.read(n)
-    if len(buf) != n:
-        raise TruncatedFileError(f"file ends inside {what} ({len(buf)} of {n} bytes)")
-    return buf
-
-
-def _remaining(f):
-    pos = f.tell()
-    end = f.seek(0, 2)
-    f.seek(pos)
-    return end - pos
-
-
-def load_weights(path) -> WeightSet:
-    with open(path, "rb") as f:
-        magic, version, kc, pc, _, n_layers = struct.unpack("<4sIBBHI", _read(f, 16, "header"))
-        if magic != _WEIGHT_MAGIC:
-            raise BadMagicError(f"bad magic {magic!r}, expected {_WEIGHT_MAGIC!r}")
-        if version != _VERSION:
-            raise UnsupportedVersionError(f"format version {version}, expected {_VERSION}")
-        if kc not in _KIND_FROM:
-            raise ShapeConsistencyError(f"unknown cell kind code {kc}")
-        if pc not in _PREC_FROM:
-            raise ShapeConsistencyError(f"unknown precision code {pc}")
-        if n_layers < 1:
-            raise ShapeConsistencyError("layer count must be >= 1")
-        kind, precision = _KIND_FROM[kc], _PREC_FROM[pc]
-        dt = _dt(precision)
-        layers, prev = [], None
-        for li in range(n_layers):
-            d_in, d_h = struct.unpack("<II", _read(f, 8, f"layer {li} header"))
-            if d_in < 1 or d_h < 1:
-                raise ShapeConsistencyError(f"layer {li} has zero dimension")
-            if kind is CellKind.SRU and d_in != d_h:
-                raise ShapeConsistencyError("SRU layer must have d_in == d_h")
-            if prev is not None and d_in != prev:
-                raise ShapeConsistencyError(f"layer {li} input width {d_in} does not match previous layer "
-                                            f"width {prev}")
-            prev = d_h
-            spec = layer_spec(kind, d_in, d_h)
-            if _remaining(f) < sum(int(np.prod(s)) for s in spec) * dt.itemsize:
-                raise TruncatedFileError(f"layer {li} payload incomplete")
-            arrays = []
-            for shape in spec:
-                n = int(np.prod(shape))
-                buf = _read(f, n * dt.itemsize, f"layer {li} data")
-                arrays.append(np.frombuffer(buf, dtype=dt).astype(PRECISIONS[precision]).reshape(shape).copy())
-            layers.append(_LAYER_CLASS[kind](*arrays))
-        if f.read(1):
-            raise ShapeConsistencyError("trailing bytes after final layer")
-    return WeightSet(kind=kind, precision=precision, layers=layers)
+                yield np.ascontiguousarray(getattr(layer, fld.name), dtype=dt).tobytes()
+    _write(path, chunks())
 
 
 def save_sequence(X: np.ndarray, path) -> None:
@@ -133,32 +95,38 @@ def save_sequence(X: np.ndarray, path) -> None:
     if X.dtype not in (np.float32, np.float64):
         raise ValueError(f"unsupported dtype {X.dtype}")
     precision = "f32" if X.dtype == np.float32 else "f64"
-    with open(path, "wb") as f:
-        f.write(struct.pack("<4sIBBHII", _SEQ_MAGIC, _VERSION, _PREC_CODES[precision], 0, 0, X.shape[0], X.shape[1]))
-        f.write(np.ascontiguousarray(X, dtype=_dt(precision)).tobytes())
+    _write(path, (_RNNX_HEADER.pack(_SEQ_MAGIC, _VERSION, _PREC_CODES[precision], 0, 0, *X.shape),
+                  np.ascontiguousarray(X, dtype=_dt(precision)).tobytes()))
+
+
+def load_weights(path) -> WeightSet:
+    """Parsed and validated by the native reader (csrc/rnnw_io.cu: sizes are
+    checked against the file before anything is allocated; failures raise
+    the reference's exception classes), then split into the layer
+    dataclasses."""
+    kind, precision, dims = weights_info(path)
+    specs = [layer_spec(kind, d_in, d_h) for d_in, d_h in dims]
+    flat = np.empty(sum(int(np.prod(s)) for spec in specs for s in spec), dtype=PRECISIONS[precision])
+    _lib.check(_lib.load().rnnb_rnnw_read(_path(path), flat.ctypes.data_as(ctypes.c_void_p), flat.size,
+                                          _lib.DT_F64 if precision == "f64" else _lib.DT_F32))
+    layers, pos = [], 0
+    for spec in specs:
+        arrays = []
+        for shape in spec:
+            n = int(np.prod(shape))
+            arrays.append(flat[pos:pos + n].reshape(shape).copy())
+            pos += n
+        layers.append(_LAYER_CLASS[kind](*arrays))
+    return WeightSet(kind=kind, precision=precision, layers=layers)
 
 
 def load_sequence(path) -> np.ndarray:
-    with open(path, "rb") as f:
-        magic, version, pc, _, _, seq_len, width = struct.unpack("<4sIBBHII", _read(f, 20, "header"))
-        if magic != _SEQ_MAGIC:
-            raise BadMagicError(f"bad magic {magic!r}, expected {_SEQ_MAGIC!r}")
-        if version != _VERSION:
-            raise UnsupportedVersionError(f"format version {version}, expected {_VERSION}")
-        if pc not in _PREC_FROM:
-            raise ShapeConsistencyError(f"unknown precision code {pc}")
-        if seq_len < 1 or width < 1:
-            raise ShapeConsistencyError("sequence dimensions must be >= 1")
-        precision = _PREC_FROM[pc]
-        dt = _dt(precision)
-        payload = seq_len * width * dt.itemsize
-        got = _remaining(f)
-        if got < payload:
-            raise TruncatedFileError(f"payload incomplete ({got} of {payload} bytes)")
-        if got > payload:
-            raise ShapeConsistencyError("trailing bytes after payload")
-        buf = _read(f, payload, "payload")
-    return np.frombuffer(buf, dtype=dt).astype(PRECISIONS[precision]).reshape(seq_len, width).copy()
+    """Native reader (rnnb_rnnx_load into host memory)."""
+    precision, seq_len, width = sequence_info(path)
+    out = np.empty((seq_len, width), dtype=PRECISIONS[precision])
+    _lib.check(_lib.load().rnnb_rnnx_load(_path(path), out.ctypes.data_as(ctypes.c_void_p),
+                                          _lib.DT_F64 if precision == "f64" else _lib.DT_F32, 0, None))
+    return out
 
 
 # ---------------------------------------------------------------------------
