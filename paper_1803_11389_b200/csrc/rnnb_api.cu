@@ -92,6 +92,9 @@ struct rnnb_stack {
   // rnnb_forward_host pipeline: copy-in / copy-out streams and per-chunk events
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev[2 * 8 + 2] = {};
+  // tcgen05 streaming: the operand-conversion stream and one event per copy-in segment
+  cudaStream_t s_cv = nullptr;
+  std::vector<cudaEvent_t> sev;
   // streaming forward_host (single-layer fp32 stacks): counters the copy
   // streams and the layer kernel hand rows through
   int* stream_ctr = nullptr;  // [0] rows of X resident, [1] kernel time-out flag, [2..] per-chunk CTA counts
@@ -236,13 +239,16 @@ int tc_mode_of(int mode) {
 }
 
 // one layer on the tcgen05 path (tc_layer.cuh)
-rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb_req,
-                            float* Hout, int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
-  Layer& ly = h->layers[li];
+// time steps per tensor-core block (3xTF32 caps blocks at 32 steps, see use_tc)
+int64_t tc_block(const rnnb_stack* h, int64_t Tb_req) {
+  return (tc_mode_of(h->mode) == TC_3XTF32 && Tb_req > 32) ? 32 : Tb_req;
+}
+
+// the MMA-operand copy of a layer input: [planes][L+1][ldop] (row 0 = x_{-1})
+rnnb_status ensure_tc_op(rnnb_stack* h, int li, int64_t L, int64_t* ldop_out) {
   const int mode = tc_mode_of(h->mode);
-  const int64_t Tb = (mode == TC_3XTF32 && Tb_req > 32) ? 32 : Tb_req;  // see use_tc
   const int es = mode == TC_BF16 ? 2 : 4;
-  const int64_t ldop = (ly.din + 7) / 8 * 8;
+  const int64_t ldop = (h->layers[li].din + 7) / 8 * 8;
   const size_t opb = (size_t)(mode == TC_3XTF32 ? 2 : 1) * (L + 1) * ldop * es;
   if (h->op_bytes < opb) {
     if (h->op) cudaFree(h->op);
@@ -251,6 +257,21 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
     CUDA_TRY(cudaMalloc(&h->op, opb));
     h->op_bytes = opb;
   }
+  *ldop_out = ldop;
+  return RNNB_OK;
+}
+
+rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb_req,
+                            float* Hout, int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
+  Layer& ly = h->layers[li];
+  const int mode = tc_mode_of(h->mode);
+  const int64_t Tb = tc_block(h, Tb_req);
+  int64_t ldop = 0;
+  rnnb_status ost = ensure_tc_op(h, li, L, &ldop);
+  if (ost != RNNB_OK) return ost;
+  // streaming (rnnb_forward_host): the operand rows are converted by the
+  // copy-in stream while this launch runs; two SMs stay free for them
+  const bool streaming = h->stream_ready != nullptr;
   const int nU = ly.Hpad128 / 128;
   const int64_t nB = (L + Tb - 1) / Tb;
   // cbuf [Hpad] (c_T scratch) | aggA, aggB, incl [nB][Hpad]: written before read
@@ -281,7 +302,8 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   }
   int* status = h->tc_status;
   ++h->tc_epoch;
-  CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s));
+  if (!streaming)
+    CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s));
   TcArgs a{};
   a.Xhw = X + ly.hw_off;
   a.ldhw = ldx;
@@ -310,7 +332,14 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.nB = (int)nB;
   a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
   int grid = 0;
-  cudaError_t e = tc_layer_run(h->kind, mode, a, ly.Wtc, ly.tcKp, h->op, ldop, h->num_sms, s, &grid);
+  if (streaming) {
+    a.x_ready = h->stream_ready;
+    a.h_done = h->stream_done;
+    a.h_gran = h->stream_chunk;
+    a.stream_fail = h->stream_ctr + 1;
+  }
+  cudaError_t e = tc_layer_run(h->kind, mode, a, ly.Wtc, ly.tcKp, h->op, ldop, h->num_sms - (streaming ? 2 : 0), s,
+                               &grid);
   if (e != cudaSuccess) return cuda_fail(e, "tc_layer launch");
   if (c_io) CUDA_TRY(cudaMemcpyAsync(c_io, h->cbuf, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
   ly.last_tc = true;
@@ -567,6 +596,8 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   if (h->stream_ctr) cudaFree(h->stream_ctr);
   if (h->stream_flag_host) cudaFreeHost(h->stream_flag_host);
   if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_cv) cudaStreamDestroy(h->s_cv);
+  for (auto& e : h->sev) cudaEventDestroy(e);
   if (h->s_out) cudaStreamDestroy(h->s_out);
   delete h;
   return RNNB_OK;
@@ -795,16 +826,117 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
   }
   cudaEvent_t ev_start = h->ev[16], ev_done = h->ev[17];
 
+  StreamOps so = stream_ops();
+  const char* env_s = getenv("RNNB_HOST_STREAM");
+  // Streaming on the tcgen05 path (single-layer stacks whose T_b runs on the
+  // tensor cores): ONE layer launch on all but two SMs.  Per segment the
+  // copy-in stream lands the rows, converts them into the MMA operand on the
+  // two free SMs and bumps the operand-row counter the kernel's TMA producer
+  // waits on; each finished item counts on its output granule and the
+  // copy-out stream drains a segment once all its granules are complete.
+  const bool want_tc_stream = !h->stream_disabled.load() && !(env_s && env_s[0] == '0') && h->n_layers == 1 &&
+                              use_tc(h, T) && h->num_sms > 8;
+  if (want_tc_stream && so.write && so.wait) {
+    const int mode = tc_mode_of(h->mode);
+    const int64_t Tb = tc_block(h, T);
+    const Layer& ly = h->layers[0];
+    const int nU = ly.Hpad128 / 128;
+    // granule: whole tensor-core blocks, >= 64 steps, at most kMaxStreamChunks of them
+    int64_t g = (64 + Tb - 1) / Tb * Tb;
+    const int64_t gmin = (L + kMaxStreamChunks - 1) / kMaxStreamChunks;
+    if (g < gmin) g = (gmin + Tb - 1) / Tb * Tb;
+    const int64_t ng = (L + g - 1) / g;
+    const char* env_c = getenv("RNNB_STREAM_CHUNK");
+    const int64_t min_chunk = env_c ? atoll(env_c) : 256;
+    const int64_t sc = min_chunk > g ? (min_chunk + g - 1) / g * g : g;
+    std::vector<int64_t> seg{0};  // segment boundaries: the first granule alone, then ~sc steps
+    if (g < L) seg.push_back(g);
+    while (seg.back() + sc < L) seg.push_back(seg.back() + sc);
+    if (seg.back() < L) seg.push_back(L);
+    const int64_t nsc = (int64_t)seg.size() - 1;
+    int64_t ldop = 0;
+    if ((st = ensure_tc_op(h, 0, L, &ldop)) != RNNB_OK) return st;
+    const size_t opes = mode == TC_BF16 ? 2 : 4;
+    if (!h->stream_ctr) {
+      CUDA_TRY(cudaMalloc(&h->stream_ctr, (2 + kMaxStreamChunks) * sizeof(int)));
+      CUDA_TRY(cudaHostAlloc(&h->stream_flag_host, sizeof(int), cudaHostAllocDefault));
+    }
+    if (!h->s_cv) CUDA_TRY(cudaStreamCreateWithFlags(&h->s_cv, cudaStreamNonBlocking));
+    while ((int64_t)h->sev.size() < nsc) {
+      cudaEvent_t e;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      h->sev.push_back(e);
+    }
+    CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (2 + ng) * sizeof(int), s));
+    CUDA_TRY(cudaEventRecord(ev_start, s));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_cv, ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
+    const float* fX = reinterpret_cast<const float*>(dX);
+    const float* fXC = reinterpret_cast<const float*>(dXC);
+    // copies back to back on s_in (the copy engine never waits for a
+    // conversion); each segment's conversion + counter bump on s_cv
+    auto copy_in = [&](int64_t i) -> rnnb_status {
+      const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
+      CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice,
+                               h->s_in));
+      CUDA_TRY(cudaEventRecord(h->sev[i], h->s_in));
+      CUDA_TRY(cudaStreamWaitEvent(h->s_cv, h->sev[i], 0));
+      // operand rows t0+1 .. t0+n (row t0 = x_{t0-1}: the carry, or the
+      // previous segment's last row rewritten with the same bits)
+      const float* prev = t0 == 0 ? (h->kind == RNNB_QRNN ? fXC : nullptr) : fX + (t0 - 1) * din;
+      CUDA_TRY(tc_to_operand_rows(mode, fX + t0 * din, din, prev, static_cast<char*>(h->op) + t0 * ldop * opes,
+                                  ldop, n, (int)din, L + 1, h->s_cv));
+      CU_TRY(so.write(h->s_cv, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
+      return RNNB_OK;
+    };
+    // every segment's copy is enqueued before the layer launch: the copy
+    // engine starts at once and keeps streaming while the host encodes and
+    // launches the kernel (the kernel waits on the row counter anyway)
+    for (int64_t i = 0; i < nsc; ++i)
+      if ((st = copy_in(i)) != RNNB_OK) return st;
+    h->stream_ready = h->stream_ctr;
+    h->stream_done = h->stream_ctr + 2;
+    h->stream_chunk = (int)g;
+    st = rnnb_forward(h, dX, din, L, block_size, dH, dh, dC, dXC, stream);
+    h->stream_ready = nullptr;
+    h->stream_done = nullptr;
+    if (st != RNNB_OK) return st;
+    int64_t launches = h->last_launches + nsc;  // + the per-segment operand conversions
+    for (int64_t i = 0; i < nsc; ++i) {
+      const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
+      for (int64_t gi = t0 / g; gi * g < t0 + n; ++gi) {
+        const int64_t glen = ((gi + 1) * g < L ? (gi + 1) * g : L) - gi * g;
+        const cuuint32_t want = (cuuint32_t)(nU * ((glen + Tb - 1) / Tb));
+        CU_TRY(so.wait(h->s_out, (CUdeviceptr)(h->stream_ctr + 2 + gi), want, CU_STREAM_WAIT_VALUE_GEQ));
+      }
+      CUDA_TRY(cudaMemcpyAsync(hH + t0 * dh * es, dH + t0 * dh * es, n * dh * es, cudaMemcpyDeviceToHost, h->s_out));
+    }
+    h->last_launches = launches;
+    CUDA_TRY(cudaEventRecord(ev_done, h->s_out));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
+    CUDA_TRY(cudaEventRecord(ev_done, h->s_cv));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
+    CUDA_TRY(cudaMemcpyAsync(h->stream_flag_host, h->stream_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (*h->stream_flag_host == 0) {
+      if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
+      if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+      return st;
+    }
+    h->stream_disabled.store(true);  // rows arrived too late (serialising profiler): redo without streaming
+    return rnnb_forward_host_impl(h, X, L, block_size, H, c_state, x_carry, stream);
+  }
+
   // Streaming (single-layer fp32 stacks, warp-specialised kernel): ONE layer
   // launch consumes X while it is still being copied in -- its TMA producer
   // waits on a device counter of resident rows that the copy-in stream bumps
   // after each chunk (stream write-value) -- and each CTA counts the chunks
   // whose h rows it has stored, so the copy-out stream (stream wait-value)
   // drains chunk i while later chunks compute.
-  const char* env_s = getenv("RNNB_HOST_STREAM");
   const bool want_stream = !h->stream_disabled.load() && !(env_s && env_s[0] == '0') && h->n_layers == 1 &&
                            h->mode == RNNB_F32 && !use_tc(h, T);  // (the FFMA kernel streams; tcgen05 does not)
-  StreamOps so = stream_ops();
   if (want_stream && so.write && so.wait) {
     // The kernel counts finished h rows per granule g (whole blocks, >= 32
     // steps, at most kMaxStreamChunks granules).  Copies move segments of

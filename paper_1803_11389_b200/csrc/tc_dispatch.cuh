@@ -8,6 +8,9 @@ namespace rnnb {
 // MMA-operand copy of a layer input with a leading x_{-1} row.
 cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
                           int64_t L, int D, cudaStream_t s);
+// rows of a longer operand (3xTF32 lo plane prow rows after the hi plane)
+cudaError_t tc_to_operand_rows(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                               int64_t L, int D, int64_t prow, cudaStream_t s);
 
 // One layer on the tensor-core path.  Wtc: [3*Hpad][Kp] gate-major operand
 // weights; Xop: [L+1][ldop_in] operand input (row 0 = x_{-1}).

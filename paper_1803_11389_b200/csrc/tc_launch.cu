@@ -9,7 +9,7 @@ namespace rnnb {
 // the MMA operand type (bf16 RNE, or tf32 RNA kept in fp32 containers).
 template <int MODE>
 __global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ xcarry,
-                                  void* __restrict__ out, int64_t ldo, int64_t L, int D) {
+                                  void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow) {
   const int64_t n = (L + 1) * (int64_t)D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / D;
@@ -22,7 +22,7 @@ __global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, cons
     } else {  // 3xTF32: hi plane rows [0, L], lo plane rows [L+1, 2L+1]
       const float hi = round_x(v, XR_TF32);
       reinterpret_cast<float*>(out)[r * ldo + d] = hi;
-      reinterpret_cast<float*>(out)[(r + L + 1) * ldo + d] = round_x(v - hi, XR_TF32);
+      reinterpret_cast<float*>(out)[(r + prow) * ldo + d] = round_x(v - hi, XR_TF32);
     }
   }
 }
@@ -32,7 +32,7 @@ __global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, cons
 // ran at ~1.2 TB/s on cfg2).  Needs 16-byte aligned rows (host-checked).
 template <int MODE>
 __global__ void to_operand_v4_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ xcarry,
-                                     void* __restrict__ out, int64_t ldo, int64_t L, int D) {
+                                     void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow) {
   const int nv = D >> 2;
   for (int64_t r = blockIdx.y; r <= L; r += gridDim.y) {
     const float* src = r == 0 ? xcarry : X + (r - 1) * ldx;
@@ -52,15 +52,18 @@ __global__ void to_operand_v4_kernel(const float* __restrict__ X, int64_t ldx, c
         if (MODE == TC_3XTF32) {
           const float4 l4 = make_float4(round_x(x.x - h4.x, XR_TF32), round_x(x.y - h4.y, XR_TF32),
                                         round_x(x.z - h4.z, XR_TF32), round_x(x.w - h4.w, XR_TF32));
-          *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (r + L + 1) * ldo + d) = l4;
+          *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (r + prow) * ldo + d) = l4;
         }
       }
     }
   }
 }
 
-cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
-                          int64_t L, int D, cudaStream_t s) {
+// Operand rows 0..L of X (row r = x_{r-1}, row 0 = xcarry or zeros); the
+// 3xTF32 lo plane starts prow rows after the hi plane (prow = L+1 for a whole
+// sequence; a row range of a longer operand passes that operand's L+1).
+cudaError_t tc_to_operand_rows(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                               int64_t L, int D, int64_t prow, cudaStream_t s) {
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (D % 4 == 0 && ldx % 4 == 0 && ldo % 8 == 0 && al16(X) && (xcarry == nullptr || al16(xcarry)) && al16(out)) {
     const int nv = D / 4;
@@ -68,18 +71,23 @@ cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xc
     const int64_t rows = L + 1;
     const int by = (int)(rows < 148 * 16 / bx ? rows : (148 * 16 / bx > 0 ? 148 * 16 / bx : 1));
     const dim3 grid(bx, by);
-    if (mode == TC_BF16) to_operand_v4_kernel<TC_BF16><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
-    else if (mode == TC_TF32) to_operand_v4_kernel<TC_TF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
-    else to_operand_v4_kernel<TC_3XTF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
+    if (mode == TC_BF16) to_operand_v4_kernel<TC_BF16><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
+    else if (mode == TC_TF32) to_operand_v4_kernel<TC_TF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
+    else to_operand_v4_kernel<TC_3XTF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
     return cudaGetLastError();
   }
   const int64_t n = (L + 1) * (int64_t)D;
   const int bs = 256;
   const int grid = (int)((n + bs - 1) / bs < 148 * 16 ? (n + bs - 1) / bs : 148 * 16);
-  if (mode == TC_BF16) to_operand_kernel<TC_BF16><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
-  else if (mode == TC_TF32) to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
-  else to_operand_kernel<TC_3XTF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D);
+  if (mode == TC_BF16) to_operand_kernel<TC_BF16><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
+  else if (mode == TC_TF32) to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
+  else to_operand_kernel<TC_3XTF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
   return cudaGetLastError();
+}
+
+cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                          int64_t L, int D, cudaStream_t s) {
+  return tc_to_operand_rows(mode, X, ldx, xcarry, out, ldo, L, D, L + 1, s);
 }
 
 static bool make_map(CUtensorMap* tm, CUtensorMapDataType dt, int es, const void* base, uint64_t inner,
@@ -159,7 +167,7 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
   if (!make_map(&tx, dt, es, Xop, (uint64_t)a.D, (uint64_t)planes * (a.L + 1), (uint64_t)ldop_in, KT, N))
     return cudaErrorInvalidValue;
   const int nitems = a.nU * a.nB;
-  const int grid = nitems < num_sms ? nitems : num_sms;
+  const int grid = nitems < num_sms ? nitems : num_sms;  // (num_sms: the caller may reserve SMs)
   if (grid_out) *grid_out = grid;
   if (cell == LINEAR) {
     // dense layers: bf16 / tf32 products (fp32 layers run the FFMA kernel)

@@ -62,6 +62,14 @@ struct TcArgs {
   int nK;             // k-tiles per row (taps * Dp / KT)
   int nKtap;          // k-tiles per tap
   int nU, nB;
+  // streaming (rnnb_forward_host, single-layer stacks): the MMA operand rows
+  // are converted while the kernel runs; *x_ready = operand rows resident
+  // (sequence rows [0, *x_ready)), and each item, after its h rows are
+  // stored, adds 1 to h_done[t0 / h_gran] (nullptr: not streaming)
+  const int* x_ready;
+  int* h_done;
+  int h_gran;
+  int* stream_fail;   // set when the input did not arrive in time (see wait_rows)
   int dbg;            // RNNB_DEBUG bits, timing experiments only (results wrong): 16 no look-back,
                       // 32 no epilogue, 64 no MMAs, 128 no loads, 512 no scan/stores, 1024 no activations
 };
@@ -293,6 +301,19 @@ __device__ __forceinline__ float tc_sigmoid(float z) { return __fdividef(1.f, 1.
 // named barrier 2 over the four epilogue warps
 __device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
 
+// Streaming output: once the 128 epilogue threads stored this item's h rows
+// (ordered by the barrier), one gpu-scope fence and one count per item on
+// the item's output granule; the host's copy-out stream waits until a
+// granule holds nU x (its blocks) counts.
+__device__ __forceinline__ void tc_count_done(const TcArgs& a, int64_t t0, int et) {
+  if (a.h_done == nullptr) return;
+  tc_epi_sync();
+  if (et == 0) {
+    __threadfence();
+    atomicAdd(&a.h_done[t0 / a.h_gran], 1);
+  }
+}
+
 // Publish block b's AGGREGATE carry map, run the deterministic fixed-depth
 // look-back (composes the aggregates of blocks b-1 .. b-kLB, in fixed order,
 // onto the INCLUSIVE carry of block b-kLB-1 or c_0 -- timing never changes
@@ -418,9 +439,32 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       uint32_t it = 0;
+      uint64_t t_start = 0;
+      int rows_seen = 0;
+      bool timed_out = false;
+      if (a.x_ready) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
       for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
         const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
         const int t0 = b * a.T_b;
+        if (a.x_ready && !timed_out) {
+          // streaming input: this block's operand rows must be resident
+          // before the first x tile of the item is fetched (rows already
+          // seen need no new acquire round trip)
+          const int need = (int)((t0 + N) < a.L ? (t0 + N) : a.L);
+          while (rows_seen < need) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(rows_seen) : "l"(a.x_ready) : "memory");
+            if (rows_seen >= need) break;
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (now - t_start > kStreamTimeoutNs) {  // profiler serialising the streams: give up (host redoes)
+              atomicExch(a.stream_fail, 1);
+              timed_out = true;
+              break;
+            }
+            __nanosleep(64);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads after the acquire
+        }
         for (int kt = 0; kt < a.nK; ++kt, ++it) {
           const int s = it % C::STAGES;
           // plain try_wait (the instruction suspends in hardware): a
@@ -611,6 +655,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
         if (b == a.nB - 1 && a.c_out != nullptr && live) a.c_out[unit] = c;  // c_T of the sequence
+        tc_count_done(a, t0, et);
         continue;
       }
       const int ab = acc_it % C::NACC;
@@ -711,6 +756,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_arrive(&acc_empty[ab]);
       ++acc_it;
       if (b == a.nB - 1 && a.c_out != nullptr && unit < a.H) a.c_out[unit] = c;  // c_T of the sequence
+      tc_count_done(a, t0, et);
     }
   }
   tc_fence_before();

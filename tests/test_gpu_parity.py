@@ -550,3 +550,40 @@ def test_weight_streaming_kernel(P, oracle, kind, d, n_layers, monkeypatch):
     assert st.query(11) == 0
     assert_f32(G, whole)
     st.close()
+
+
+@pytest.mark.parametrize("kind,mode,d,L,T", [("qrnn", "f32", 1024, 2048, 32), ("qrnn", "f32", 1024, 1000, 64),
+                                             ("sru", "f32", 512, 777, 16), ("qrnn", "bf16", 1024, 2048, 64),
+                                             ("sru", "bf16", 256, 130, 1), ("qrnn", "tf32", 512, 9000, 32)])
+def test_host_streaming_tensor_core_matches_device(P, oracle, kind, mode, d, L, T, monkeypatch):
+    """rnnb_forward_host on the tcgen05 path: one layer launch on all but two
+    SMs while the copy-in stream lands rows and converts them into the MMA
+    operand (an operand-row counter the TMA producer waits on), copy-out per
+    granule of finished items -- bitwise the device call (the look-back's
+    fixed order makes the result independent of the item schedule), with
+    carried c / x_carry; the chunked fallback within the look-back bound."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 1, 73, np.float32)
+    X = np.random.default_rng(20).standard_normal((L, d)).astype(np.float32)
+    st = P.DeviceStack(kind, layers, mode=mode)
+    c0 = np.random.default_rng(21).standard_normal(d).astype(np.float32)
+    x0 = np.random.default_rng(22).standard_normal(d).astype(np.float32)
+    cd, xd = torch.from_numpy(c0.copy()).cuda(), torch.from_numpy(x0.copy()).cuda()
+    ref = st.forward(torch.from_numpy(X).cuda(), T, c_state=cd, x_carry=xd if kind == "qrnn" else None)
+    ref = ref.cpu().numpy()
+    assert st.query(9) == 1
+    for stream in ("1", "0"):
+        monkeypatch.setenv("RNNB_HOST_STREAM", stream)
+        c, x = c0.copy(), x0.copy()
+        H = st.forward_host(X, T, c_state=c, x_carry=x if kind == "qrnn" else None)
+        if stream == "1":
+            assert H.tobytes() == ref.tobytes()
+            assert c.tobytes() == cd.cpu().numpy().tobytes()
+        else:
+            assert normwise(H, ref) <= 1e-6
+        if kind == "qrnn":
+            assert x.tobytes() == xd.cpu().numpy().tobytes()
+        H2 = st.forward_host(X, T)  # zero state, twice (counter reuse)
+        H3 = st.forward_host(X, T)
+        assert H2.tobytes() == H3.tobytes()
+    st.close()
