@@ -761,7 +761,9 @@ def main():
     ap.add_argument("--partition", choices=("replicas", "pipeline", "hidden"), default="replicas",
                     help="replicas: N independent copies of the workload (cfg1/cfg2 do not shard); "
                          "pipeline: cfg4 layer pipeline across ranks; hidden: cfg5 hidden sharding")
-    ap.add_argument("--chunk", type=int, default=1024, help="pipeline chunk (steps, a multiple of --block)")
+    ap.add_argument("--chunk", type=int, default=2048,
+                    help="pipeline chunk (steps, a multiple of --block); 2048 balances the per-chunk launch cost "
+                         "against the (G-1)/n bubble: profiles/pipeline_chunks_r2.json")
     ap.add_argument("--no-partitioned", dest="partitioned", action="store_false",
                     help="skip the cfg4 pipeline / cfg5 hidden-sharding sub-object")
     ap.add_argument("--no-configs", dest="configs", action="store_false",
