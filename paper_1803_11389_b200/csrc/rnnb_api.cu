@@ -84,6 +84,8 @@ struct rnnb_stack {
   int tc_epoch = 0;       // launch tag of the look-back status words
   int* tc_status = nullptr;  // [capacity] status words, cleared only on (re)allocation
   size_t tc_status_n = 0;
+  float* fix = nullptr;      // 3xTF32 split last wave: first halves' chunk sums
+  size_t fix_bytes = 0;
   int* flags = nullptr;
   size_t cf_bytes = 0;
   void* hostX = nullptr;  // e2e device staging
@@ -289,13 +291,15 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   // (re)allocated: each launch tags its statuses 4*epoch + state, so anything
   // an earlier launch left (any layer, any layout) reads as "not yet"
   const size_t nst = (size_t)nB * nU;
-  if (h->tc_status_n < nst || h->tc_epoch >= (1 << 28)) {
-    if (h->tc_status_n < nst) {
+  // + kFixSlots words after the look-back statuses: the split last wave's flags
+  constexpr size_t kFixSlots = 128;
+  if (h->tc_status_n < nst + kFixSlots || h->tc_epoch >= (1 << 28)) {
+    if (h->tc_status_n < nst + kFixSlots) {
       if (h->tc_status) cudaFree(h->tc_status);
       h->tc_status = nullptr;
       h->tc_status_n = 0;
-      CUDA_TRY(cudaMalloc(&h->tc_status, nst * sizeof(int)));
-      h->tc_status_n = nst;
+      CUDA_TRY(cudaMalloc(&h->tc_status, (nst + kFixSlots) * sizeof(int)));
+      h->tc_status_n = nst + kFixSlots;
     }
     CUDA_TRY(cudaMemsetAsync(h->tc_status, 0, h->tc_status_n * sizeof(int), s));
     h->tc_epoch = 0;
@@ -331,6 +335,29 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.nU = nU;
   a.nB = (int)nB;
   a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
+  // 3xTF32: split the last, partial wave's items in two K halves on two CTAs
+  // (tc_work in tc_layer.cuh; the arithmetic is the same split or not)
+  const int nitems = nU * (int)nB;
+  const int G = nitems < h->num_sms - (streaming ? 2 : 0) ? nitems : h->num_sms - (streaming ? 2 : 0);
+  a.split_start = nitems;
+  const char* env_sp = getenv("RNNB_TC_SPLIT");
+  if (mode == TC_3XTF32 && !(env_sp && env_sp[0] == '0')) {
+    const int W = nitems / G, R = nitems - W * G;
+    const int nch = (a.nK + 3) / 4;
+    if (W >= 1 && R > 0 && 2 * R <= G && R <= (int)kFixSlots && nch >= 2) {
+      const size_t fb = (size_t)R * 3 * tc_pick_n((int)Tb) * 128 * sizeof(float);
+      if (h->fix_bytes < fb) {
+        if (h->fix) cudaFree(h->fix);
+        h->fix = nullptr;
+        h->fix_bytes = 0;
+        CUDA_TRY(cudaMalloc(&h->fix, fb));
+        h->fix_bytes = fb;
+      }
+      a.split_start = W * G;
+      a.fix = h->fix;
+      a.fixflag = status + (h->tc_status_n - kFixSlots);
+    }
+  }
   int grid = 0;
   if (streaming) {
     a.x_ready = h->stream_ready;
@@ -587,6 +614,7 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   if (h->rev) cudaFree(h->rev);
   if (h->cbuf) cudaFree(h->cbuf);
   if (h->tc_status) cudaFree(h->tc_status);
+  if (h->fix) cudaFree(h->fix);
   for (auto& p : h->ws)
     if (p) cudaFree(p);
   if (h->hostX) cudaFree(h->hostX);

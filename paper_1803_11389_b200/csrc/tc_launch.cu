@@ -168,6 +168,8 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
     return cudaErrorInvalidValue;
   const int nitems = a.nU * a.nB;
   const int grid = nitems < num_sms ? nitems : num_sms;  // (num_sms: the caller may reserve SMs)
+  // no split last wave unless the caller set one up (zero-initialised args)
+  if (a.split_start <= 0 || a.split_start > nitems || mode != TC_3XTF32) a.split_start = nitems;
   if (grid_out) *grid_out = grid;
   if (cell == LINEAR) {
     // dense layers: bf16 / tf32 products (fp32 layers run the FFMA kernel)

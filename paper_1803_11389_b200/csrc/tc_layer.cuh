@@ -70,6 +70,12 @@ struct TcArgs {
   int* h_done;
   int h_gran;
   int* stream_fail;   // set when the input did not arrive in time (see wait_rows)
+  // 3xTF32 only: items from split_start on (the last, partial wave) are
+  // split in two halves on two CTAs (see tc_work); fix holds the first
+  // halves' K-chunk sums [slot][3N][128], fixflag their release tags
+  int split_start;
+  float* fix;
+  int* fixflag;
   int dbg;            // RNNB_DEBUG bits, timing experiments only (results wrong): 16 no look-back,
                       // 32 no epilogue, 64 no MMAs, 128 no loads, 512 no scan/stores, 1024 no activations
 };
@@ -390,10 +396,41 @@ struct TcCfg {
   static constexpr bool CHUNKED = MODE == TC_3XTF32;
   static constexpr int CK = 4;
   static_assert(!CHUNKED || (N <= 32 && NACC == 2), "chunked accumulation keeps 3N partials in registers");
-  static constexpr int TMEM_COLS = (NACC * ACC_COLS <= 32) ? 32 : (NACC * ACC_COLS <= 64) ? 64
-                                   : (NACC * ACC_COLS <= 128) ? 128 : (NACC * ACC_COLS <= 256) ? 256 : 512;
+  // 3xTF32: ACC_COLS more columns stash the first half's chunk sum (see the epilogue)
+  static constexpr int USED_COLS = NACC * ACC_COLS + (CHUNKED ? ACC_COLS : 0);
+  static constexpr int TMEM_COLS = (USED_COLS <= 32) ? 32 : (USED_COLS <= 64) ? 64
+                                   : (USED_COLS <= 128) ? 128 : (USED_COLS <= 256) ? 256 : 512;
+  static_assert(USED_COLS <= 512, "TMEM holds 512 columns");
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
+
+// This CTA's k-th unit of work.  Whole items blockIdx.x + k*grid below
+// a.split_start (round-robin, time-block-major, as before); then, when the
+// last wave is split (3xTF32 only; the host guarantees 2R <= grid for its R
+// items), one half of a last-wave item: part 0 = K chunks [0, nch/2) whose
+// sum goes to the fixup buffer, part 1 = chunks [nch/2, nch), which finishes
+// the item.  Every item -- split or not -- sums its chunks as
+// S = (chunks [0, nch/2)) + (chunks [nch/2, nch)), so the split never
+// changes a bit of the result and any grid gives the same numbers.
+struct TcWork {
+  int item, kt0, kt1, part;  // part: -1 whole item, 0 / 1 halves
+};
+template <int CK>
+__device__ __forceinline__ bool tc_work(const TcArgs& a, int nitems, int k, TcWork& w) {
+  const int bx = blockIdx.x, G = gridDim.x;
+  const int nwhole = a.split_start > bx ? (a.split_start - bx + G - 1) / G : 0;
+  if (k < nwhole) {
+    w = TcWork{bx + k * G, 0, a.nK, -1};
+    return true;
+  }
+  if (k == nwhole && a.split_start < nitems && bx < 2 * (nitems - a.split_start)) {
+    const int kmid = ((a.nK + CK - 1) / CK / 2) * CK;
+    const int part = bx & 1;
+    w = TcWork{a.split_start + bx / 2, part ? kmid : 0, part ? a.nK : kmid, part};
+    return true;
+  }
+  return false;
+}
 
 template <int CELL, int MODE, int N>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -443,7 +480,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int rows_seen = 0;
       bool timed_out = false;
       if (a.x_ready) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      TcWork w;
+      for (int k = 0; tc_work<C::CK>(a, nitems, k, w); ++k) {
+        const int item = w.item;
         const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
         const int t0 = b * a.T_b;
         if (a.x_ready && !timed_out) {
@@ -465,7 +504,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads after the acquire
         }
-        for (int kt = 0; kt < a.nK; ++kt, ++it) {
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % C::STAGES;
           // plain try_wait (the instruction suspends in hardware): a
           // nanosleep back-off here overshot the stage release by up to ~1 us
@@ -498,14 +537,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     "tc_issue_ktile hard-codes 16 KB gate tiles and 4 K-steps of 32 B");
       constexpr int HALF = 3 * C::A_BYTES + C::B_BYTES;  // hi -> lo plane offset (3xTF32)
       uint32_t it = 0, acc_it = 0;
-      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      TcWork w;
+      for (int k = 0; tc_work<C::CK>(a, nitems, k, w); ++k) {
         int ab = acc_it % C::NACC;
         uint32_t dbase = tmem + ab * C::ACC_COLS;
         if (!C::CHUNKED) {
           mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
           tc_fence_after();
         }
-        for (int kt = 0; kt < a.nK; ++kt, ++it) {
+        for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int kc = C::CHUNKED ? kt % C::CK : kt;  // k-tile index inside the accumulation
           if (C::CHUNKED && kc == 0) {  // a new K-chunk accumulates into a fresh buffer
             ab = acc_it % C::NACC;
@@ -521,7 +561,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc_issue_ktile<MODE>(dbase, sw128_desc(st), sw128_desc(st + 3 * C::A_BYTES), idesc, kc != 0, N,
                                  (uint64_t)(HALF >> 4));
           tc_commit_elect(&empty[s]);  // frees the smem stage once these MMAs have read it
-          if (C::CHUNKED && (kc == C::CK - 1 || kt == a.nK - 1)) {
+          if (C::CHUNKED && (kc == C::CK - 1 || kt == w.kt1 - 1)) {
             tc_commit_elect(&acc_full[ab]);  // this K-chunk's partial products complete
             ++acc_it;
           }
@@ -545,13 +585,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int row = q * 32 + lane;          // unit within the tile
     const int et = threadIdx.x - 64;        // 0..127
     uint32_t acc_it = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    TcWork w;
+    for (int k = 0; tc_work<C::CK>(a, nitems, k, w); ++k) {
+      const int item = w.item;
       const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
       const int64_t t0 = (int64_t)b * a.T_b;
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       const int unit = u * 128 + row;
       if (a.dbg & 32) {  // timing experiment: epilogue only hands the accumulators back
-        const int nacc = C::CHUNKED ? (a.nK + C::CK - 1) / C::CK : 1;
+        const int nacc = C::CHUNKED ? (w.kt1 - w.kt0 + C::CK - 1) / C::CK : 1;
         for (int ch = 0; ch < nacc; ++ch, ++acc_it) {
           const int ab = acc_it % C::NACC;
           mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
@@ -599,7 +641,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
         for (int j = 0; j < N; ++j) rz[j] = rf[j] = ro[j] = 0.f;
         const int nch = (a.nK + C::CK - 1) / C::CK;
-        for (int ch = 0; ch < nch; ++ch, ++acc_it) {
+        const int hch = nch / 2;  // first chunk of the second half (see tc_work)
+        const int c_lo = w.part == 1 ? hch : 0, c_hi = w.part == 0 ? hch : nch;
+        // the first half's sum waits in TMEM columns past the accumulators
+        const uint32_t stash = tmem + C::NACC * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
+        for (int ch = c_lo; ch < c_hi; ++ch, ++acc_it) {
+          if (w.part < 0 && ch == hch && hch > 0) {  // whole item: set the first half aside
+#pragma unroll
+            for (int c0 = 0; c0 < N; c0 += 16) {
+              tmem_st16(stash + 0 * N + c0, *reinterpret_cast<float(*)[16]>(rz + c0));
+              tmem_st16(stash + 1 * N + c0, *reinterpret_cast<float(*)[16]>(rf + c0));
+              tmem_st16(stash + 2 * N + c0, *reinterpret_cast<float(*)[16]>(ro + c0));
+            }
+            tmem_st_wait();
+#pragma unroll
+            for (int j = 0; j < N; ++j) rz[j] = rf[j] = ro[j] = 0.f;
+          }
           const int ab = acc_it % C::NACC;
           mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
           tc_fence_after();
@@ -619,6 +676,42 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
           tc_fence_before();
           mbar_arrive(&acc_empty[ab]);
+        }
+        const int slot = item - a.split_start;
+        if (w.part == 0) {  // first half of a split item: hand the sum on, nothing else
+          float* fx = a.fix + (size_t)slot * 3 * N * 128 + row;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            fx[(size_t)(0 * N + j) * 128] = rz[j];
+            fx[(size_t)(1 * N + j) * 128] = rf[j];
+            fx[(size_t)(2 * N + j) * 128] = ro[j];
+          }
+          tc_epi_sync();
+          if (et == 0) st_release(&a.fixflag[slot], 4 * a.epoch + 3);
+          continue;
+        }
+        if (w.part == 1) {  // second half: S = (first half, from the other CTA) + this half
+          if (et == 0) while (ld_acquire(&a.fixflag[slot]) < 4 * a.epoch + 3) __nanosleep(64);
+          tc_epi_sync();
+          const float* fx = a.fix + (size_t)slot * 3 * N * 128 + row;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            rz[j] = __ldcg(fx + (size_t)(0 * N + j) * 128) + rz[j];
+            rf[j] = __ldcg(fx + (size_t)(1 * N + j) * 128) + rf[j];
+            ro[j] = __ldcg(fx + (size_t)(2 * N + j) * 128) + ro[j];
+          }
+        } else if (hch > 0) {  // whole item: S = (stashed first half) + second half
+#pragma unroll
+          for (int c0 = 0; c0 < N; c0 += 16) {
+            float sz[16], sf[16], so[16];
+            tmem_ld_gates16(stash + 0 * N + c0, stash + 1 * N + c0, stash + 2 * N + c0, sz, sf, so);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              rz[c0 + j] = sz[j] + rz[c0 + j];
+              rf[c0 + j] = sf[j] + rf[c0 + j];
+              ro[c0 + j] = so[j] + ro[c0 + j];
+            }
+          }
         }
 #pragma unroll
         for (int j = 0; j < N; ++j) {

@@ -587,3 +587,24 @@ def test_host_streaming_tensor_core_matches_device(P, oracle, kind, mode, d, L, 
         H3 = st.forward_host(X, T)
         assert H2.tobytes() == H3.tobytes()
     st.close()
+
+
+@pytest.mark.parametrize("kind,d,L", [("qrnn", 1024, 2048), ("sru", 1024, 3000), ("qrnn", 2048, 700)])
+def test_split_last_wave_is_bitwise_neutral(P, oracle, kind, d, L, monkeypatch):
+    """3xTF32: the last partial wave's items run as two K halves on two CTAs
+    (first half's chunk sum handed over through global memory); every item
+    sums (first half) + (second half), so the split changes no bit
+    (RNNB_TC_SPLIT=0 disables it) -- and the result stays within the fp32
+    bound of the oracle."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 1, 79, np.float32)
+    X = np.random.default_rng(23).standard_normal((L, d)).astype(np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    st = P.DeviceStack(kind, layers, mode="f32")
+    split = st.forward(Xd, 32).cpu().numpy()
+    assert st.query(9) == 1
+    monkeypatch.setenv("RNNB_TC_SPLIT", "0")
+    whole = st.forward(Xd, 32).cpu().numpy()
+    assert split.tobytes() == whole.tobytes()
+    assert_f32(split, oracle.run_blocked(kind, layers, X, 32))
+    st.close()
