@@ -451,6 +451,25 @@ def run_ours(args, rank, world, local_rank):
             blk = 32 if part == "pipeline" else 64
             partitioned[part] = run_partitioned(args, rank, world, local_rank, workload=wl, partition=part,
                                                 mode="bf16", block=blk, chunk=args.chunk)
+    # the reference-facing drop-in call (run_blocked, blocked.py:221-268):
+    # host arrays in and out, and -- as the reference re-stacks its weights
+    # on every call -- a full weight upload/repack per call
+    dropin = None
+    if rank == 0 and args.dropin:
+        cfg_ = P.RnnConfig(w.kind, int(w.X.shape[1]), int(w.layers[-1].d_h), n_layers=len(w.layers),
+                           precision="f32")
+        ws_ = P.WeightSet(w.kind, "f32", w.layers)
+        Xf = np.ascontiguousarray(w.X, np.float32)
+        P.run_blocked(cfg_, ws_, Xf, args.block)
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            P.run_blocked(cfg_, ws_, Xf, args.block)
+            ts.append((time.perf_counter() - t0) * 1e3)
+        dms = statistics.median(ts)
+        dropin = {"value": round(L / (dms / 1e3), 1), "unit": UNIT, "ms_per_call": round(dms, 3),
+                  "api": "paper_1803_11389_b200.run_blocked (reference signature; weights uploaded and "
+                         "repacked on every call, as the reference re-stacks them)"}
     if rank != 0:
         st.close()
         return None
@@ -503,6 +522,8 @@ def run_ours(args, rank, world, local_rank):
         "modes": {m: sweep_of(r, m) for m, r in extra.items()},
         "clocks": head["clocks"],
     }
+    if dropin:
+        line["dropin"] = dropin
     if partitioned:
         line["partitioned"] = partitioned
     if args.configs and world == 1:
@@ -764,6 +785,8 @@ def main():
     ap.add_argument("--chunk", type=int, default=2048,
                     help="pipeline chunk (steps, a multiple of --block); 2048 balances the per-chunk launch cost "
                          "against the (G-1)/n bubble: profiles/pipeline_chunks_r2.json")
+    ap.add_argument("--no-dropin", dest="dropin", action="store_false",
+                    help="skip timing the reference-signature run_blocked call")
     ap.add_argument("--no-partitioned", dest="partitioned", action="store_false",
                     help="skip the cfg4 pipeline / cfg5 hidden-sharding sub-object")
     ap.add_argument("--no-configs", dest="configs", action="store_false",

@@ -236,6 +236,17 @@ bool use_tc(const rnnb_stack* h, int64_t Tb) {
   return false;
 }
 
+// fp32 mode: the tcgen05 path only when its items fill the GPU (a short
+// sequence of a narrow layer -- cfg1: 4 unit tiles x 16 blocks = 64 items --
+// runs faster on the FFMA kernel's 128+ CTAs)
+bool use_tc_layer(const rnnb_stack* h, const Layer& ly, int64_t L, int64_t Tb) {
+  if (!use_tc(h, Tb)) return false;
+  if (h->mode != RNNB_F32) return true;
+  const int64_t Tbe = Tb > 32 ? 32 : Tb;
+  const int64_t items = (ly.dh + 127) / 128 * ((L + Tbe - 1) / Tbe);
+  return items >= h->num_sms;
+}
+
 int tc_mode_of(int mode) {
   return mode == RNNB_BF16 ? TC_BF16 : (mode == RNNB_TF32 ? TC_TF32 : TC_3XTF32);  // f32, f32x3: 3xTF32
 }
@@ -383,7 +394,7 @@ rnnb_status layer_launch(rnnb_stack* h, int li, const TA* X, int64_t ldx, int64_
                          TA* Hout, int64_t ldh, TA* c_io, TA* xc_io, TA* G, int64_t ldg,
                          cudaStream_t s) {
   if constexpr (sizeof(TA) == 4) {
-    if (G == nullptr && use_tc(h, Tb))
+    if (G == nullptr && use_tc_layer(h, h->layers[li], L, Tb))
       return tc_layer_launch(h, li, reinterpret_cast<const float*>(X), ldx, L, Tb, reinterpret_cast<float*>(Hout),
                              ldh, reinterpret_cast<float*>(c_io), reinterpret_cast<float*>(xc_io), s);
   }
@@ -447,7 +458,7 @@ __global__ void reverse_rows_kernel(const T* __restrict__ X, int64_t ldx, T* __r
 template <typename TA, typename TW>
 rnnb_status forward_t(rnnb_stack* h, const TA* X, int64_t ldx, int64_t L, int64_t Tb, TA* H,
                       int64_t ldh, TA* c_state, TA* x_carry, cudaStream_t s) {
-  if (ldx < 0 && !(sizeof(TA) == 4 && use_tc(h, Tb))) {
+  if (ldx < 0 && !(sizeof(TA) == 4 && use_tc_layer(h, h->layers[0], L, Tb))) {
     // Time-reversed input (the backward direction of a bidirectional stack).
     // The tcgen05 path reads it directly: its operand conversion walks the
     // rows with the negative stride.  The FFMA kernels fetch x with TMA
@@ -863,7 +874,7 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
   // waits on; each finished item counts on its output granule and the
   // copy-out stream drains a segment once all its granules are complete.
   const bool want_tc_stream = !h->stream_disabled.load() && !(env_s && env_s[0] == '0') && h->n_layers == 1 &&
-                              use_tc(h, T) && h->num_sms > 8;
+                              use_tc_layer(h, h->layers[0], L, T) && h->num_sms > 8;
   if (want_tc_stream && so.write && so.wait) {
     const int mode = tc_mode_of(h->mode);
     const int64_t Tb = tc_block(h, T);
@@ -964,7 +975,7 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
   // whose h rows it has stored, so the copy-out stream (stream wait-value)
   // drains chunk i while later chunks compute.
   const bool want_stream = !h->stream_disabled.load() && !(env_s && env_s[0] == '0') && h->n_layers == 1 &&
-                           h->mode == RNNB_F32 && !use_tc(h, T);  // (the FFMA kernel streams; tcgen05 does not)
+                           h->mode == RNNB_F32 && !use_tc_layer(h, h->layers[0], L, T);  // FFMA streaming
   if (want_stream && so.write && so.wait) {
     // The kernel counts finished h rows per granule g (whole blocks, >= 32
     // steps, at most kMaxStreamChunks granules).  Copies move segments of

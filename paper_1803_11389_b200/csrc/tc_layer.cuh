@@ -371,9 +371,14 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
     Aacc = Aacc * Aj[k];
   }
   const float cin = Aacc * anchor + Bacc;
-  a.incl[sidx] = Ablk * cin + Bblk;
-  tc_epi_sync();
-  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
+  // the INCLUSIVE carry is only ever read as the anchor of block b+kLB+1:
+  // the last kLB+1 blocks skip its store, barrier and release (one gpu-scope
+  // fence and an L2 round trip per item; every block of a cfg2 T_b=64 launch)
+  if (b + kLB + 1 < a.nB) {
+    a.incl[sidx] = Ablk * cin + Bblk;
+    tc_epi_sync();
+    if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
+  }
   return cin;
 }
 
@@ -388,7 +393,10 @@ struct TcCfg {
                                 : (3 * STAGE_BYTES + 2048 <= 227 * 1024) ? 3
                                                                           : 2;
   static constexpr int ACC_COLS = 3 * N;
-  static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;
+  // accumulator buffers in TMEM: up to 4 for the non-chunked modes (N <= 32:
+  // the MMA warp runs up to three items ahead of an epilogue held up in the
+  // look-back), 2 for 3xTF32 (alternating K chunks) and N = 64
+  static constexpr int NACC = CHUNKED ? 2 : (4 * ACC_COLS <= 512) ? 4 : (2 * ACC_COLS <= 512) ? 2 : 1;
   // 3xTF32: the tensor cores' fp32 accumulation error grows linearly with the
   // reduction length (measured), so K is accumulated in CK-k-tile chunks
   // (K = 128) in alternating TMEM buffers and the chunk partials are summed
@@ -441,8 +449,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(tsm + (size_t)C::STAGES * C::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* acc_full = empty + C::STAGES;
-  uint64_t* acc_empty = acc_full + 2;
-  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  uint64_t* acc_empty = acc_full + 4;
+  uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nitems = a.nU * a.nB;
@@ -452,7 +460,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::NACC; ++i) {
       mbar_init(&acc_full[i], 1);
       mbar_init(&acc_empty[i], 128);
     }
