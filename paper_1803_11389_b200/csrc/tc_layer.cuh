@@ -396,7 +396,7 @@ struct TcCfg {
   // accumulator buffers in TMEM: up to 4 for the non-chunked modes (N <= 32:
   // the MMA warp runs up to three items ahead of an epilogue held up in the
   // look-back), 2 for 3xTF32 (alternating K chunks) and N = 64
-  static constexpr int NACC = CHUNKED ? 2 : (4 * ACC_COLS <= 512) ? 4 : (2 * ACC_COLS <= 512) ? 2 : 1;
+  static constexpr int NACC = MODE == TC_3XTF32 ? 2 : (4 * ACC_COLS <= 512) ? 4 : (2 * ACC_COLS <= 512) ? 2 : 1;
   // 3xTF32: the tensor cores' fp32 accumulation error grows linearly with the
   // reduction length (measured), so K is accumulated in CK-k-tile chunks
   // (K = 128) in alternating TMEM buffers and the chunk partials are summed
