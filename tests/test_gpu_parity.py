@@ -580,7 +580,9 @@ def test_host_streaming_tensor_core_matches_device(P, oracle, kind, mode, d, L, 
             assert H.tobytes() == ref.tobytes()
             assert c.tobytes() == cd.cpu().numpy().tobytes()
         else:
-            assert normwise(H, ref) <= 1e-6
+            # chunked fallback: the look-back re-anchors at chunk edges, and an
+            # fp32 chunk too short to fill the GPU runs on the FFMA kernel
+            assert normwise(H, ref) <= (1e-5 if mode == "f32" else 1e-6)
         if kind == "qrnn":
             assert x.tobytes() == xd.cpu().numpy().tobytes()
         H2 = st.forward_host(X, T)  # zero state, twice (counter reuse)
