@@ -886,11 +886,13 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     if (g < gmin) g = (gmin + Tb - 1) / Tb * Tb;
     const int64_t ng = (L + g - 1) / g;
     const char* env_c = getenv("RNNB_STREAM_CHUNK");
-    const int64_t min_chunk = env_c ? atoll(env_c) : 256;
+    const int64_t min_chunk = env_c ? atoll(env_c) : 512;
     const int64_t sc = min_chunk > g ? (min_chunk + g - 1) / g * g : g;
-    std::vector<int64_t> seg{0};  // segment boundaries: the first granule alone, then ~sc steps
+    // segment boundaries: the first granule alone (the kernel starts on it),
+    // then segments doubling up to ~sc steps (fewer host operations)
+    std::vector<int64_t> seg{0};
     if (g < L) seg.push_back(g);
-    while (seg.back() + sc < L) seg.push_back(seg.back() + sc);
+    for (int64_t len = 2 * g; seg.back() + len < L; len = len * 2 < sc ? len * 2 : sc) seg.push_back(seg.back() + len);
     if (seg.back() < L) seg.push_back(L);
     const int64_t nsc = (int64_t)seg.size() - 1;
     int64_t ldop = 0;
@@ -929,10 +931,13 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       CU_TRY(so.write(h->s_cv, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
       return RNNB_OK;
     };
-    // every segment's copy is enqueued before the layer launch: the copy
-    // engine starts at once and keeps streaming while the host encodes and
-    // launches the kernel (the kernel waits on the row counter anyway)
-    for (int64_t i = 0; i < nsc; ++i)
+    // the first segments' copies are enqueued before the layer launch (the
+    // copy engine starts at once and stays busy while the host encodes and
+    // launches the kernel, which waits on the row counter anyway), the rest
+    // after it (each segment costs the host a copy, an event, a conversion
+    // launch and a write-value: enqueuing them all first delayed the launch)
+    const int64_t pre = nsc < 3 ? nsc : 3;
+    for (int64_t i = 0; i < pre; ++i)
       if ((st = copy_in(i)) != RNNB_OK) return st;
     h->stream_ready = h->stream_ctr;
     h->stream_done = h->stream_ctr + 2;
@@ -941,6 +946,8 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     h->stream_ready = nullptr;
     h->stream_done = nullptr;
     if (st != RNNB_OK) return st;
+    for (int64_t i = pre; i < nsc; ++i)
+      if ((st = copy_in(i)) != RNNB_OK) return st;
     int64_t launches = h->last_launches + nsc;  // + the per-segment operand conversions
     for (int64_t i = 0; i < nsc; ++i) {
       const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
