@@ -181,7 +181,7 @@ def cfg4(oracle):
     return w, mats, xp, ref, cref
 
 
-@pytest.mark.parametrize("mode", ["f32_ffma", "f32", "bf16", "f32x3"])
+@pytest.mark.parametrize("mode", ["f32_ffma", "f32", "bf16", "tf32", "f32x3"])
 def test_cfg4_all_layers_prefix(P, oracle, cfg4, mode, monkeypatch):
     """8 x QRNN-2048 on an 8192-step prefix, T_b=32: output and every
     layer's c_T vs the fp32 oracle (fp32 bound for the fp32 modes: the
@@ -207,10 +207,10 @@ def test_cfg4_all_layers_prefix(P, oracle, cfg4, mode, monkeypatch):
     _record(f"cfg4 {mode} 8 layers L={PREFIX4} vs fp32 oracle", e)
     for li in range(8):
         _record(f"cfg4 {mode} layer {li + 1} c_T vs fp32 oracle", normwise(cs[li], cref[li]))
-    if mode == "bf16":
-        assert e <= BOUND_VS_F32["bf16"]
+    if mode in ("bf16", "tf32"):
+        assert e <= BOUND_VS_F32[mode]
         for li in range(8):
-            assert normwise(cs[li], cref[li]) <= BOUND_VS_F32["bf16"]
+            assert normwise(cs[li], cref[li]) <= BOUND_VS_F32[mode]
     else:
         assert_f32(H, ref, mode)
         for li in range(8):
@@ -371,3 +371,27 @@ def test_cfg5_bidirectional_wide_sru(P, oracle, cfg5, T):
             r.close()
         del got, ranks
         torch.cuda.empty_cache()
+
+
+def test_cfg5_fp32_mode_wide_layers(P, oracle, cfg5):
+    """cfg5's shape in fp32 mode (3xTF32 tcgen05 at T_b = 64): layer 1 of each
+    direction vs the fp32 oracle, layer 2 (d_in 8192) vs the float64 cell on
+    a prefix / suffix of the GPU's own layer input, all at the fp32 bound."""
+    import torch
+    w = cfg5
+    Hd, L = 4096, w.X.shape[0]
+    ins, outs = _bidir_layers(P, type(w)(w.name, w.kind, w.layers[:2], w.X, w.block_sizes,
+                                         bidirectional=True, layers_bwd=w.layers_bwd[:2]), "f32", 64)
+    y1 = outs[0].cpu().numpy()
+    ref_f = oracle.layer_blocked("sru", list(w.layers[0].mats()), w.X, 32)[0]
+    ref_b = oracle.layer_blocked("sru", list(w.layers_bwd[0].mats()), np.ascontiguousarray(w.X[::-1]), 32)[0]
+    _record("cfg5 f32 layer 1 fwd vs fp32 oracle", assert_f32(y1[:, :Hd], ref_f))
+    _record("cfg5 f32 layer 1 bwd vs fp32 oracle", assert_f32(y1[:, Hd:], ref_b[::-1]))
+    x = ins[1].cpu().numpy()
+    y = outs[1].cpu().numpy()
+    rf = sru_wide_f64(list(w.layers[1].mats()), x, x[:, :Hd], rows=EDGE5)
+    rb = sru_wide_f64(list(w.layers_bwd[1].mats()), np.ascontiguousarray(x[::-1][:EDGE5]), x[::-1][:EDGE5, Hd:])[::-1]
+    _record("cfg5 f32 layer 2 fwd prefix vs f64 cell", assert_f32(y[:EDGE5, :Hd], rf))
+    _record("cfg5 f32 layer 2 bwd suffix vs f64 cell", assert_f32(y[L - EDGE5:, Hd:], rb))
+    del ins, outs
+    torch.cuda.empty_cache()
