@@ -181,7 +181,7 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
         KT, es, kstep = (64, 2, 16) if mode == "bf16" else (32, 4, 8)
         planes = 2 if x3 else 1
         floor_cyc, floor_src = mma_floor_cycles("f16" if mode == "bf16" else "tf32")
-        cyc = max(floor_cyc, N / 2)
+        cyc = max(floor_cyc, (2 * N if x3 else N) / 2)
         n_instr = 0.0
         l2_bytes = 0.0
         taps = 2 if w.kind.value == "qrnn" else 1
@@ -189,7 +189,8 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
             nU = -(-lay.d_h // 128)
             nK = taps * -(-lay.d_in // KT)
             nB = -(-L // T_eff)
-            n_instr += nU * nB * nK * 3 * (KT // kstep) * (3 if x3 else 1)
+            # 3xTF32 issues 2 MMAs per gate and K-step: W_hi.[x_hi | x_lo] (N' = 2N) + W_lo.x_hi
+            n_instr += nU * nB * nK * 3 * (KT // kstep) * (2 if x3 else 1)
             l2_bytes += nU * nB * nK * planes * (3 * 128 + N) * KT * es
         n_instr /= launches_per_step
         l2_bytes /= launches_per_step

@@ -145,27 +145,32 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
 #define RNNB_KTILE(KIND)                                                                            \
   "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b;\n\t.reg .b32 d;\n\telect.sync _|e, 0xffffffff;\n\t" \
   "setp.ne.b32 p, %4, 0;\n\t" RNNB_GATE(KIND, 0) RNNB_GATE(KIND, 1) RNNB_GATE(KIND, 2) "}\n"
-// 3xTF32: per K-step hi.hi (starts with acc), hi.lo, lo.hi; the lo planes sit
-// %6 (16-byte units) after the hi planes
-#define RNNB_X3STEP(ACCP)                                                                   \
-  "@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, b, %3, " ACCP ";\n\t"                    \
-  "add.s64 bl, b, %6;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, bl, %3, 1;\n\t"   \
-  "add.s64 al, a, %6;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [d], al, b, %3, 1;\n\t"
+// 3xTF32 in TWO MMAs per gate and K-step instead of three: the x tile holds
+// [x_hi ; x_lo] as 2N rows, so W_hi . [x_hi | x_lo] is ONE N' = 2N MMA (idesc
+// %3) writing hi.hi to accumulator columns [0, N) and hi.lo to [N, 2N); then
+// W_lo . x_hi (N columns, idesc %6) accumulates into [N, 2N).  The issue floor
+// is ~51 cycles per MMA for any N <= 64, so this is 1.5x fewer issue slots;
+// the epilogue adds the two column halves.  W_lo = W_hi + 3 tiles (%5 =
+// 3*16 KB in 16-byte units); gate g: accumulator d0 + 2N*g (%7 = 2N).
+#define RNNB_X3STEP(ACCP)                                                          \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, b, %3, " ACCP ";\n\t"           \
+  "add.s64 al, a, %5;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [dc], al, b, %6, 1;\n\t"
 #define RNNB_X3NEXT "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t" RNNB_X3STEP("1")
-#define RNNB_X3GATE(G) \
-  "add.s64 a, %1, " #G "*1024;\n\tmov.b64 b, %2;\n\tmad.lo.s32 d, %5, " #G ", %0;\n\t" RNNB_X3STEP("p") RNNB_X3NEXT RNNB_X3NEXT RNNB_X3NEXT
+#define RNNB_X3GATE(G)                                                                            \
+  "add.s64 a, %1, " #G "*1024;\n\tmov.b64 b, %2;\n\tmad.lo.s32 d, %7, " #G ", %0;\n\t"         \
+  "shr.u32 dc, %7, 1;\n\tadd.s32 dc, d, dc;\n\t" RNNB_X3STEP("p") RNNB_X3NEXT RNNB_X3NEXT RNNB_X3NEXT
 template <int MODE>
 __device__ __forceinline__ void tc_issue_ktile(uint32_t d0, uint64_t a0, uint64_t b0, uint32_t idesc, uint32_t acc,
-                                               uint32_t n, uint64_t lo16) {
+                                               uint32_t n, uint32_t idesc_n, uint64_t lo16) {
   if constexpr (MODE == TC_BF16)
-    asm volatile(RNNB_KTILE("f16") ::"r"(d0), "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n), "l"(lo16));
+    asm volatile(RNNB_KTILE("f16") ::"r"(d0), "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n));
   else if constexpr (MODE == TC_TF32)
-    asm volatile(RNNB_KTILE("tf32") ::"r"(d0), "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n), "l"(lo16));
-  else
+    asm volatile(RNNB_KTILE("tf32") ::"r"(d0), "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n));
+  else  // idesc: N' = 2n (W_hi . [x_hi | x_lo]); idesc_n: N = n (W_lo . x_hi)
     asm volatile(
-        "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b, al, bl;\n\t.reg .b32 d;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b, al;\n\t.reg .b32 d, dc;\n\telect.sync _|e, 0xffffffff;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t" RNNB_X3GATE(0) RNNB_X3GATE(1) RNNB_X3GATE(2) "}\n" ::"r"(d0),
-        "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "r"(n), "l"(lo16));
+        "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "l"(lo16), "r"(idesc_n), "r"(2 * n));
 }
 #undef RNNB_MMA
 #undef RNNB_KSTEP
@@ -388,11 +393,17 @@ struct TcCfg {
   static constexpr int A_BYTES = 128 * 128;  // one gate tile: 128 rows x 128 B
   static constexpr int B_BYTES = N * 128;
   static constexpr int SPLIT = MODE == TC_3XTF32 ? 2 : 1;  // hi (+ lo) planes per operand
+  // stage layout: A tiles [plane][gate] (plane 0 = hi), then the x tile of
+  // every plane stacked as ONE B tile of SPLIT*N rows ([x_hi ; x_lo]: the
+  // 3xTF32 MMA W_hi . [x_hi | x_lo] reads both planes as N' = 2N columns)
+  static constexpr int B_OFF = SPLIT * 3 * A_BYTES;
   static constexpr int STAGE_BYTES = SPLIT * (3 * A_BYTES + B_BYTES);
   static constexpr int STAGES = (4 * STAGE_BYTES + 2048 <= 227 * 1024)   ? 4
                                 : (3 * STAGE_BYTES + 2048 <= 227 * 1024) ? 3
                                                                           : 2;
-  static constexpr int ACC_COLS = 3 * N;
+  // accumulator columns per gate: N, or for 3xTF32 2N ([hi.hi | hi.lo + lo.hi])
+  static constexpr int GCOLS = (MODE == TC_3XTF32 ? 2 : 1) * N;
+  static constexpr int ACC_COLS = 3 * GCOLS;
   // accumulator buffers in TMEM: up to 4 for the non-chunked modes (N <= 32:
   // the MMA warp runs up to three items ahead of an epilogue held up in the
   // look-back), 2 for 3xTF32 (alternating K chunks) and N = 64
@@ -404,8 +415,8 @@ struct TcCfg {
   static constexpr bool CHUNKED = MODE == TC_3XTF32;
   static constexpr int CK = 4;
   static_assert(!CHUNKED || (N <= 32 && NACC == 2), "chunked accumulation keeps 3N partials in registers");
-  // 3xTF32: ACC_COLS more columns stash the first half's chunk sum (see the epilogue)
-  static constexpr int USED_COLS = NACC * ACC_COLS + (CHUNKED ? ACC_COLS : 0);
+  // 3xTF32: 3N more columns stash the first half's chunk sum (see the epilogue)
+  static constexpr int USED_COLS = NACC * ACC_COLS + (CHUNKED ? 3 * N : 0);
   static constexpr int TMEM_COLS = (USED_COLS <= 32) ? 32 : (USED_COLS <= 64) ? 64
                                    : (USED_COLS <= 128) ? 128 : (USED_COLS <= 256) ? 256 : 512;
   static_assert(USED_COLS <= 512, "TMEM holds 512 columns");
@@ -528,11 +539,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const int kx = (kt - tap * a.nKtap) * C::KT;
 #pragma unroll
           for (int p = 0; p < C::SPLIT; ++p) {  // hi plane, then lo plane (3xTF32)
-            unsigned char* sp = st + p * (3 * C::A_BYTES + C::B_BYTES);
             for (int g = 0; g < 3; ++g)
-              tma_load_2d(sp + g * C::A_BYTES, &tmW, kt * C::KT, (p * 3 + g) * a.Hpad + u * 128, &full[s]);
+              tma_load_2d(st + (p * 3 + g) * C::A_BYTES, &tmW, kt * C::KT, (p * 3 + g) * a.Hpad + u * 128,
+                          &full[s]);
             // operand row r holds x_{r-1}: block rows t0.. for tap 0, t0-1.. for tap 1
-            tma_load_2d(sp + 3 * C::A_BYTES, &tmX, kx, (int)(p * (a.L + 1)) + t0 + 1 - tap, &full[s]);
+            tma_load_2d(st + C::B_OFF + p * C::B_BYTES, &tmX, kx, (int)(p * (a.L + 1)) + t0 + 1 - tap, &full[s]);
           }
         }
       }
@@ -543,7 +554,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       constexpr uint32_t idesc = tc_idesc<MODE>(128, N);
       static_assert(C::A_BYTES == 16384 && C::KT / C::UK == 4 && (C::UK * C::ES) == 32,
                     "tc_issue_ktile hard-codes 16 KB gate tiles and 4 K-steps of 32 B");
-      constexpr int HALF = 3 * C::A_BYTES + C::B_BYTES;  // hi -> lo plane offset (3xTF32)
+      constexpr uint32_t idesc_n = tc_idesc<MODE>(128, N);
+      constexpr uint32_t idesc_2n = tc_idesc<MODE>(128, C::SPLIT * N);  // 3xTF32: [x_hi | x_lo]
       uint32_t it = 0, acc_it = 0;
       TcWork w;
       for (int k = 0; tc_work<C::CK>(a, nitems, k, w); ++k) {
@@ -566,8 +578,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc_fence_after();
           unsigned char* st = tsm + (size_t)s * C::STAGE_BYTES;
           if (!(a.dbg & 64))  // dbg 64 (timing): no MMAs
-            tc_issue_ktile<MODE>(dbase, sw128_desc(st), sw128_desc(st + 3 * C::A_BYTES), idesc, kc != 0, N,
-                                 (uint64_t)(HALF >> 4));
+            tc_issue_ktile<MODE>(dbase, sw128_desc(st), sw128_desc(st + C::B_OFF),
+                                 C::CHUNKED ? idesc_2n : idesc, kc != 0, N, idesc_n,
+                                 (uint64_t)((3 * C::A_BYTES) >> 4));
           tc_commit_elect(&empty[s]);  // frees the smem stage once these MMAs have read it
           if (C::CHUNKED && (kc == C::CK - 1 || kt == w.kt1 - 1)) {
             tc_commit_elect(&acc_full[ab]);  // this K-chunk's partial products complete
@@ -671,15 +684,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           const uint32_t tb = tmem + ab * C::ACC_COLS + ((uint32_t)(q * 32) << 16);
 #pragma unroll
           for (int c0 = 0; c0 < N; c0 += 16) {
-            float pz[16], pf[16], po[16];
-            tmem_ld16(tb + 0 * N + c0, pz);
-            tmem_ld16(tb + 1 * N + c0, pf);
-            tmem_ld16(tb + 2 * N + c0, po);
+            // per gate: columns [0, N) hi.hi, [N, 2N) hi.lo + lo.hi
+            float pz[16], pf[16], po[16], cz[16], cf[16], co[16];
+            tmem_ld_gates16(tb + 0 * C::GCOLS + c0, tb + 1 * C::GCOLS + c0, tb + 2 * C::GCOLS + c0, pz, pf, po);
+            tmem_ld_gates16(tb + 0 * C::GCOLS + N + c0, tb + 1 * C::GCOLS + N + c0, tb + 2 * C::GCOLS + N + c0, cz,
+                            cf, co);
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              rz[c0 + j] += pz[j];
-              rf[c0 + j] += pf[j];
-              ro[c0 + j] += po[j];
+              rz[c0 + j] += pz[j] + cz[j];
+              rf[c0 + j] += pf[j] + cf[j];
+              ro[c0 + j] += po[j] + co[j];
             }
           }
           tc_fence_before();
