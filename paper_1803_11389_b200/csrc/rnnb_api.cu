@@ -354,7 +354,7 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   const char* env_sp = getenv("RNNB_TC_SPLIT");
   if (mode == TC_3XTF32 && !(env_sp && env_sp[0] == '0')) {
     const int W = nitems / G, R = nitems - W * G;
-    const int nch = (a.nK + 3) / 4;
+    const int nch = (a.nK + RNNB_X3_CK - 1) / RNNB_X3_CK;
     if (W >= 1 && R > 0 && 2 * R <= G && R <= (int)kFixSlots && nch >= 2) {
       const size_t fb = (size_t)R * 3 * tc_pick_n((int)Tb) * 128 * sizeof(float);
       if (h->fix_bytes < fb) {

@@ -387,6 +387,9 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
   return cin;
 }
 
+#ifndef RNNB_X3_CK
+#define RNNB_X3_CK 8  // 3xTF32 K chunk in k-tiles (8 x 32 = 256-deep; 128-deep: 8 % slower, half the error)
+#endif
 template <int MODE, int N>
 struct TcCfg {
   static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
@@ -413,7 +416,7 @@ struct TcCfg {
   // (K = 128) in alternating TMEM buffers and the chunk partials are summed
   // in fp32 registers by the epilogue (keeps 3xTF32 inside the fp32 bound)
   static constexpr bool CHUNKED = MODE == TC_3XTF32;
-  static constexpr int CK = 4;
+  static constexpr int CK = RNNB_X3_CK;
   static_assert(!CHUNKED || (N <= 32 && NACC == 2), "chunked accumulation keeps 3N partials in registers");
   // 3xTF32: 3N more columns stash the first half's chunk sum (see the epilogue)
   static constexpr int USED_COLS = NACC * ACC_COLS + (CHUNKED ? 3 * N : 0);
