@@ -92,7 +92,7 @@ struct rnnb_stack {
   void* hostH = nullptr;
   size_t hx_bytes = 0, hh_bytes = 0;
   // rnnb_forward_host pipeline: copy-in / copy-out streams and per-chunk events
-  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaStream_t s_in = nullptr, s_in2 = nullptr, s_out = nullptr;
   cudaEvent_t ev[2 * 8 + 2] = {};
   // tcgen05 streaming: the operand-conversion stream and one event per copy-in segment
   cudaStream_t s_cv = nullptr;
@@ -104,6 +104,11 @@ struct rnnb_stack {
   const int* stream_ready = nullptr;
   int* stream_done = nullptr;
   int stream_chunk = 0;
+  unsigned long long* stream_trace = nullptr;  // RNNB_STREAM_TRACE: in-kernel time stamps (tuning)
+  int* stream_flags = nullptr;  // tcgen05 streaming conversion: per-group flags (epoch-tagged)
+  size_t stream_flags_n = 0;
+  int stream_epoch = 0;
+  int stream_free_sms = 2;  // SMs the streaming layer launch leaves to the operand conversion
   bool stream_refused = false;
   // set after a streaming time-out (a serialising profiler, a stalled copy
   // engine): later rnnb_forward_host calls on this handle use the chunked
@@ -274,6 +279,52 @@ rnnb_status ensure_tc_op(rnnb_stack* h, int li, int64_t L, int64_t* ldop_out) {
   return RNNB_OK;
 }
 
+// + kFixSlots words after the look-back statuses: the split last wave's flags
+constexpr size_t kFixSlots = 128;
+
+// Scratch of one tensor-core layer launch, (re)allocated when too small.
+// cudaMalloc / cudaFree wait for the device, so the streaming host path calls
+// this BEFORE it launches anything that spins on rows still to be enqueued.
+rnnb_status tc_layer_scratch(rnnb_stack* h, Layer& ly, int64_t nB, int nU, int N, bool x3, cudaStream_t s) {
+  // cbuf [Hpad] (c_T scratch) | aggA, aggB, incl [nB][Hpad]: written before read
+  const size_t plane = (size_t)nB * ly.Hpad128;
+  const size_t cfb = ((size_t)ly.Hpad128 + 3 * plane) * sizeof(float);
+  if (h->cf_bytes < cfb) {
+    if (h->cbuf) cudaFree(h->cbuf);
+    h->cbuf = nullptr;
+    h->cf_bytes = 0;
+    CUDA_TRY(cudaMalloc(&h->cbuf, cfb));
+    h->cf_bytes = cfb;
+  }
+  // status words [nB][nU] in their own allocation, cleared only when it is
+  // (re)allocated: each launch tags its statuses 4*epoch + state, so anything
+  // an earlier launch left (any layer, any layout) reads as "not yet"
+  const size_t nst = (size_t)nB * nU;
+  // + kFixSlots words after the look-back statuses: the split last wave's flags
+  if (h->tc_status_n < nst + kFixSlots || h->tc_epoch >= (1 << 28)) {
+    if (h->tc_status_n < nst + kFixSlots) {
+      if (h->tc_status) cudaFree(h->tc_status);
+      h->tc_status = nullptr;
+      h->tc_status_n = 0;
+      CUDA_TRY(cudaMalloc(&h->tc_status, (nst + kFixSlots) * sizeof(int)));
+      h->tc_status_n = nst + kFixSlots;
+    }
+    CUDA_TRY(cudaMemsetAsync(h->tc_status, 0, h->tc_status_n * sizeof(int), s));
+    h->tc_epoch = 0;
+  }
+  if (x3) {
+    const size_t fb = kFixSlots * 3 * (size_t)N * 128 * sizeof(float);
+    if (h->fix_bytes < fb) {
+      if (h->fix) cudaFree(h->fix);
+      h->fix = nullptr;
+      h->fix_bytes = 0;
+      CUDA_TRY(cudaMalloc(&h->fix, fb));
+      h->fix_bytes = fb;
+    }
+  }
+  return RNNB_OK;
+}
+
 rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, int64_t L, int64_t Tb_req,
                             float* Hout, int64_t ldh, float* c_io, float* xc_io, cudaStream_t s) {
   Layer& ly = h->layers[li];
@@ -287,34 +338,12 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   const bool streaming = h->stream_ready != nullptr;
   const int nU = ly.Hpad128 / 128;
   const int64_t nB = (L + Tb - 1) / Tb;
-  // cbuf [Hpad] (c_T scratch) | aggA, aggB, incl [nB][Hpad]: written before read
+  rnnb_status sst = tc_layer_scratch(h, ly, nB, nU, tc_pick_n((int)Tb), mode == TC_3XTF32, s);
+  if (sst != RNNB_OK) return sst;
   const size_t plane = (size_t)nB * ly.Hpad128;
-  const size_t cfb = ((size_t)ly.Hpad128 + 3 * plane) * sizeof(float);
-  if (h->cf_bytes < cfb) {
-    if (h->cbuf) cudaFree(h->cbuf);
-    h->cbuf = nullptr;
-    h->cf_bytes = 0;
-    CUDA_TRY(cudaMalloc(&h->cbuf, cfb));
-    h->cf_bytes = cfb;
-  }
   float* aggA = h->cbuf + ly.Hpad128;
-  // status words [nB][nU] in their own allocation, cleared only when it is
-  // (re)allocated: each launch tags its statuses 4*epoch + state, so anything
-  // an earlier launch left (any layer, any layout) reads as "not yet"
   const size_t nst = (size_t)nB * nU;
-  // + kFixSlots words after the look-back statuses: the split last wave's flags
-  constexpr size_t kFixSlots = 128;
-  if (h->tc_status_n < nst + kFixSlots || h->tc_epoch >= (1 << 28)) {
-    if (h->tc_status_n < nst + kFixSlots) {
-      if (h->tc_status) cudaFree(h->tc_status);
-      h->tc_status = nullptr;
-      h->tc_status_n = 0;
-      CUDA_TRY(cudaMalloc(&h->tc_status, (nst + kFixSlots) * sizeof(int)));
-      h->tc_status_n = nst + kFixSlots;
-    }
-    CUDA_TRY(cudaMemsetAsync(h->tc_status, 0, h->tc_status_n * sizeof(int), s));
-    h->tc_epoch = 0;
-  }
+  (void)nst;
   int* status = h->tc_status;
   ++h->tc_epoch;
   if (!streaming)
@@ -349,22 +378,21 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   // 3xTF32: split the last, partial wave's items in two K halves on two CTAs
   // (tc_work in tc_layer.cuh; the arithmetic is the same split or not)
   const int nitems = nU * (int)nB;
-  const int G = nitems < h->num_sms - (streaming ? 2 : 0) ? nitems : h->num_sms - (streaming ? 2 : 0);
+  const int G = nitems < h->num_sms - (streaming ? h->stream_free_sms : 0) ? nitems : h->num_sms - (streaming ? h->stream_free_sms : 0);
   a.split_start = nitems;
   const char* env_sp = getenv("RNNB_TC_SPLIT");
   if (mode == TC_3XTF32 && !(env_sp && env_sp[0] == '0')) {
-    const int W = nitems / G, R = nitems - W * G;
+    int W = nitems / G, R = nitems - W * G;
     const int nch = (a.nK + RNNB_X3_CK - 1) / RNNB_X3_CK;
+    if (streaming && nitems > G) {
+      // input-bound launch (rows arrive slower than the kernel consumes them):
+      // what counts is how soon the LAST blocks finish after their rows land,
+      // so the last G/2 items are split whatever the wave structure
+      R = G / 2 < (int)kFixSlots ? G / 2 : (int)kFixSlots;
+      W = 1;
+    }
     if (W >= 1 && R > 0 && 2 * R <= G && R <= (int)kFixSlots && nch >= 2) {
-      const size_t fb = (size_t)R * 3 * tc_pick_n((int)Tb) * 128 * sizeof(float);
-      if (h->fix_bytes < fb) {
-        if (h->fix) cudaFree(h->fix);
-        h->fix = nullptr;
-        h->fix_bytes = 0;
-        CUDA_TRY(cudaMalloc(&h->fix, fb));
-        h->fix_bytes = fb;
-      }
-      a.split_start = W * G;
+      a.split_start = nitems - R;
       a.fix = h->fix;
       a.fixflag = status + (h->tc_status_n - kFixSlots);
     }
@@ -374,9 +402,10 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
     a.x_ready = h->stream_ready;
     a.h_done = h->stream_done;
     a.h_gran = h->stream_chunk;
+    a.trace = h->stream_trace;
     a.stream_fail = h->stream_ctr + 1;
   }
-  cudaError_t e = tc_layer_run(h->kind, mode, a, ly.Wtc, ly.tcKp, h->op, ldop, h->num_sms - (streaming ? 2 : 0), s,
+  cudaError_t e = tc_layer_run(h->kind, mode, a, ly.Wtc, ly.tcKp, h->op, ldop, h->num_sms - (streaming ? h->stream_free_sms : 0), s,
                                &grid);
   if (e != cudaSuccess) return cuda_fail(e, "tc_layer launch");
   if (c_io) CUDA_TRY(cudaMemcpyAsync(c_io, h->cbuf, ly.dh * sizeof(float), cudaMemcpyDeviceToDevice, s));
@@ -633,8 +662,10 @@ rnnb_status rnnb_stack_destroy(rnnb_stack_t h) {
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
   if (h->stream_ctr) cudaFree(h->stream_ctr);
+  if (h->stream_flags) cudaFree(h->stream_flags);
   if (h->stream_flag_host) cudaFreeHost(h->stream_flag_host);
   if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->s_in2) cudaStreamDestroy(h->s_in2);
   if (h->s_cv) cudaStreamDestroy(h->s_cv);
   for (auto& e : h->sev) cudaEventDestroy(e);
   if (h->s_out) cudaStreamDestroy(h->s_out);
@@ -886,7 +917,8 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     if (g < gmin) g = (gmin + Tb - 1) / Tb * Tb;
     const int64_t ng = (L + g - 1) / g;
     const char* env_c = getenv("RNNB_STREAM_CHUNK");
-    const int64_t min_chunk = env_c ? atoll(env_c) : 512;
+    int64_t min_chunk = env_c ? atoll(env_c) : 256;
+    if (min_chunk * (kMaxSegs - 8) < L) min_chunk = (L + kMaxSegs - 9) / (kMaxSegs - 8);  // at most kMaxSegs segments
     const int64_t sc = min_chunk > g ? (min_chunk + g - 1) / g * g : g;
     // segment boundaries: the first granule alone (the kernel starts on it),
     // then segments doubling up to ~sc steps (fewer host operations)
@@ -899,28 +931,110 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     if ((st = ensure_tc_op(h, 0, L, &ldop)) != RNNB_OK) return st;
     const size_t opes = mode == TC_BF16 ? 2 : 4;
     if (!h->stream_ctr) {
-      CUDA_TRY(cudaMalloc(&h->stream_ctr, (2 + kMaxStreamChunks) * sizeof(int)));
+      CUDA_TRY(cudaMalloc(&h->stream_ctr, (4 + kMaxStreamChunks + kMaxSegs) * sizeof(int)));
       CUDA_TRY(cudaHostAlloc(&h->stream_flag_host, sizeof(int), cudaHostAllocDefault));
     }
     if (!h->s_cv) CUDA_TRY(cudaStreamCreateWithFlags(&h->s_cv, cudaStreamNonBlocking));
+    if (!h->s_in2) CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in2, cudaStreamNonBlocking));
+    if (nsc > kMaxSegs) return fail(RNNB_EINVAL, "streaming segment plan too long");
     while ((int64_t)h->sev.size() < nsc) {
       cudaEvent_t e;
       CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       h->sev.push_back(e);
     }
-    CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (2 + ng) * sizeof(int), s));
+    CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (4 + kMaxStreamChunks + kMaxSegs) * sizeof(int), s));
     CUDA_TRY(cudaEventRecord(ev_start, s));
     CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_in2, ev_start, 0));
     CUDA_TRY(cudaStreamWaitEvent(h->s_cv, ev_start, 0));
     CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
     const float* fX = reinterpret_cast<const float*>(dX);
     const float* fXC = reinterpret_cast<const float*>(dXC);
-    // copies back to back on s_in (the copy engine never waits for a
-    // conversion); each segment's conversion + counter bump on s_cv
+    // Output straight into the caller's buffer when it is pinned (mapped)
+    // host memory: the epilogue's h stores go over PCIe as posted writes
+    // while later items compute -- no copy-out segments, no wait-value
+    // operations, and nothing left to copy after the kernel ends.  Measured
+    // (tools/zc_probe.cu): SM stores to pinned memory 50 GB/s, and they run
+    // full duplex with the copy engine's H2D (8 MB each way in 187 us);
+    // SM *reads* of pinned memory do not overlap with writes (290-320 us),
+    // so the input keeps the copy engine.
+    char* dHz = nullptr;
+    {
+      const char* env_z = getenv("RNNB_ZC_OUT");
+      cudaPointerAttributes pa;
+      if (!(env_z && env_z[0] == '0') && cudaPointerGetAttributes(&pa, H) == cudaSuccess &&
+          pa.type == cudaMemoryTypeHost && pa.devicePointer != nullptr)
+        dHz = static_cast<char*>(pa.devicePointer);
+      else
+        (void)cudaGetLastError();
+    }
+    // RNNB_STREAM_TRACE=1: timing events after every copy / conversion and
+    // around the layer kernel, printed relative to the call's start (tuning only)
+    const bool trace = getenv("RNNB_STREAM_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    std::vector<std::string> tname;
+    const bool trace_ev = trace && atoi(getenv("RNNB_STREAM_TRACE")) >= 2;  // 2: + stream events (they slow the call)
+    auto mark = [&](cudaStream_t ms, const std::string& name) {
+      if (!trace_ev) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, ms);
+      tev.push_back(e);
+      tname.push_back(name);
+    };
+    mark(s, "start");
+    const int64_t nBt = (L + Tb - 1) / Tb;
+    if (trace) {
+      if (h->stream_trace) cudaFree(h->stream_trace);
+      CUDA_TRY(cudaMalloc(&h->stream_trace, (1 + 2 * nBt) * sizeof(unsigned long long)));
+      CUDA_TRY(cudaMemset(h->stream_trace, 0, (1 + 2 * nBt) * sizeof(unsigned long long)));
+    } else if (h->stream_trace) {
+      cudaFree(h->stream_trace);
+      h->stream_trace = nullptr;
+    }
+    // ONE persistent conversion launch (s_cv, on the SMs the layer kernel
+    // leaves free) follows the copy engine: per segment the host only
+    // enqueues the copy and a write-value of the rows landed; the conversion
+    // kernel polls that counter and publishes the operand-row counter the
+    // layer kernel's TMA producer waits on (tc_launch.cu).  Unaligned inputs
+    // keep one conversion launch per segment.
+    const char* env_f = getenv("RNNB_STREAM_SMS");
+    h->stream_free_sms = env_f ? atoi(env_f) : 2;
+    if (h->stream_free_sms < 1) h->stream_free_sms = 1;
+    if (h->stream_free_sms > 16) h->stream_free_sms = 16;
+    int* copied_ctr = h->stream_ctr + 2 + kMaxStreamChunks;  // [+1]: the conversion workers' group queue
+    int* seg_flag = h->stream_ctr + 4 + kMaxStreamChunks;    // per copy segment: epoch once it has landed
+    TcSegTab segtab{};
+    segtab.n = (int)nsc;
+    for (int64_t i = 0; i < nsc; ++i) segtab.end[i] = (int)seg[i + 1];
+    // per-group "converted" flags tagged with a per-call epoch (never cleared
+    // per call); (re)allocated here, before anything of this call is launched
+    if (h->stream_flags_n < (size_t)L + 1 || h->stream_epoch >= (1 << 30)) {
+      if (h->stream_flags_n < (size_t)L + 1) {
+        if (h->stream_flags) cudaFree(h->stream_flags);
+        h->stream_flags = nullptr;
+        h->stream_flags_n = 0;
+        CUDA_TRY(cudaMalloc(&h->stream_flags, ((size_t)L + 1) * sizeof(int)));
+        h->stream_flags_n = (size_t)L + 1;
+      }
+      CUDA_TRY(cudaMemsetAsync(h->stream_flags, 0, h->stream_flags_n * sizeof(int), s));
+      h->stream_epoch = 0;
+    }
+    ++h->stream_epoch;
+    const bool conv_stream = tc_to_operand_stream_ok(fX, din, h->kind == RNNB_QRNN ? fXC : nullptr, h->op, ldop, (int)din);
     auto copy_in = [&](int64_t i) -> rnnb_status {
       const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
-      CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice,
-                               h->s_in));
+      // segments alternate between two copy streams: a stream's write-value
+      // runs only after its copy has fully landed, and on ONE stream the next
+      // copy waited for it -- a ~30 us bubble per segment boundary (in-kernel
+      // time stamps: rows arrived at 33 GB/s instead of PCIe's 53)
+      cudaStream_t sc_in = conv_stream && (i & 1) ? h->s_in2 : h->s_in;
+      CUDA_TRY(cudaMemcpyAsync(dX + t0 * din * es, hX + t0 * din * es, n * din * es, cudaMemcpyHostToDevice, sc_in));
+      mark(sc_in, "copied rows " + std::to_string(t0 + n));
+      if (conv_stream) {
+        CU_TRY(so.write(sc_in, (CUdeviceptr)(seg_flag + i), (cuuint32_t)h->stream_epoch, 0));
+        return RNNB_OK;
+      }
       CUDA_TRY(cudaEventRecord(h->sev[i], h->s_in));
       CUDA_TRY(cudaStreamWaitEvent(h->s_cv, h->sev[i], 0));
       // operand rows t0+1 .. t0+n (row t0 = x_{t0-1}: the carry, or the
@@ -929,27 +1043,48 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       CUDA_TRY(tc_to_operand_rows(mode, fX + t0 * din, din, prev, static_cast<char*>(h->op) + t0 * ldop * opes,
                                   ldop, n, (int)din, L + 1, h->s_cv));
       CU_TRY(so.write(h->s_cv, (CUdeviceptr)h->stream_ctr, (cuuint32_t)(t0 + n), 0));
+      mark(h->s_cv, "converted rows " + std::to_string(t0 + n));
       return RNNB_OK;
     };
     // the first segments' copies are enqueued before the layer launch (the
     // copy engine starts at once and stays busy while the host encodes and
     // launches the kernel, which waits on the row counter anyway), the rest
-    // after it (each segment costs the host a copy, an event, a conversion
-    // launch and a write-value: enqueuing them all first delayed the launch)
-    const int64_t pre = nsc < 3 ? nsc : 3;
+    // after it
+    const char* env_p = getenv("RNNB_STREAM_PRE");
+    const int64_t want_pre = env_p ? atoll(env_p) : 3;
+    const int64_t pre = nsc < want_pre ? nsc : want_pre;
     for (int64_t i = 0; i < pre; ++i)
       if ((st = copy_in(i)) != RNNB_OK) return st;
     h->stream_ready = h->stream_ctr;
-    h->stream_done = h->stream_ctr + 2;
+    h->stream_done = dHz ? nullptr : h->stream_ctr + 2;
     h->stream_chunk = (int)g;
-    st = rnnb_forward(h, dX, din, L, block_size, dH, dh, dC, dXC, stream);
+    mark(s, "before layer kernel");
+    st = rnnb_forward(h, dX, din, L, block_size, dHz ? dHz : dH, dh, dC, dXC, stream);
+    mark(s, "layer kernel done");
+    // the persistent conversion goes AFTER the layer launch: rnnb_forward may
+    // (re)allocate scratch, and cudaMalloc / cudaFree wait for the device --
+    // a conversion kernel already spinning on rows the host has not enqueued
+    // yet would hold that wait until its time-out
+    if (st == RNNB_OK && conv_stream) {
+      const char* env_g = getenv("RNNB_STREAM_GROUP");
+      int group = env_g ? atoi(env_g) : 16;
+      if (group < 1) group = 16;
+      const char* env_n = getenv("RNNB_STREAM_CTAS");
+      int workers = env_n ? atoi(env_n) : 12;
+      if (workers < 1) workers = 1;
+      CUDA_TRY(tc_to_operand_stream(mode, fX, din, h->kind == RNNB_QRNN ? fXC : nullptr, h->op, ldop, L, (int)din,
+                                    segtab, seg_flag, h->stream_ctr, h->stream_ctr + 1, h->stream_flags, copied_ctr + 1,
+                                    h->stream_epoch,
+                                    group, workers, h->s_cv));
+      mark(h->s_cv, "conversion kernel done");
+    }
     h->stream_ready = nullptr;
     h->stream_done = nullptr;
     if (st != RNNB_OK) return st;
     for (int64_t i = pre; i < nsc; ++i)
       if ((st = copy_in(i)) != RNNB_OK) return st;
     int64_t launches = h->last_launches + nsc;  // + the per-segment operand conversions
-    for (int64_t i = 0; i < nsc; ++i) {
+    for (int64_t i = 0; i < nsc && !dHz; ++i) {
       const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
       for (int64_t gi = t0 / g; gi * g < t0 + n; ++gi) {
         const int64_t glen = ((gi + 1) * g < L ? (gi + 1) * g : L) - gi * g;
@@ -963,13 +1098,40 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
     CUDA_TRY(cudaEventRecord(ev_done, h->s_cv));
     CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
+    CUDA_TRY(cudaEventRecord(ev_done, h->s_in));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
+    CUDA_TRY(cudaEventRecord(ev_done, h->s_in2));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
     CUDA_TRY(cudaMemcpyAsync(h->stream_flag_host, h->stream_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    mark(s, "all done");
     CUDA_TRY(cudaStreamSynchronize(s));
+    if (trace) {
+      for (size_t i = 1; trace_ev && i < tev.size(); ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[0], tev[i]);
+        fprintf(stderr, "[rnnb stream trace] %8.1f us  %s\n", ms * 1e3, tname[i].c_str());
+      }
+      for (auto e : tev) cudaEventDestroy(e);
+      std::vector<unsigned long long> tr(1 + 2 * nBt);
+      cudaMemcpy(tr.data(), h->stream_trace, tr.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+      for (int64_t b = 0; b < nBt; b += (nBt > 16 ? nBt / 16 : 1))
+        fprintf(stderr, "[rnnb stream trace] block %4lld: rows seen %8.1f us, stored %8.1f us after kernel start\n",
+                (long long)b, (double)(tr[1 + b] - tr[0]) * 1e-3, (double)(tr[1 + nBt + b] - tr[0]) * 1e-3);
+      fprintf(stderr, "[rnnb stream trace] last block: rows seen %8.1f us, stored %8.1f us\n",
+              (double)(tr[nBt] - tr[0]) * 1e-3, (double)(tr[2 * nBt] - tr[0]) * 1e-3);
+    }
     if (*h->stream_flag_host == 0) {
       if (c_state) CUDA_TRY(cudaMemcpyAsync(c_state, dC, csz * es, cudaMemcpyDeviceToHost, s));
       if (x_carry) CUDA_TRY(cudaMemcpyAsync(x_carry, dXC, xsz * es, cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
       return st;
+    }
+    if (getenv("RNNB_STREAM_DEBUG")) {
+      int c[3] = {0, 0, 0};
+      cudaMemcpy(&c[0], h->stream_ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost);
+      cudaMemcpy(&c[2], copied_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[rnnb] tcgen05 host streaming gave up: ready=%d fail=%d groups claimed=%d (L=%lld)\n", c[0], c[1], c[2],
+              (long long)L);
     }
     h->stream_disabled.store(true);  // rows arrived too late (serialising profiler): redo without streaming
     return rnnb_forward_host_impl(h, X, L, block_size, H, c_state, x_carry, stream);
@@ -1008,7 +1170,7 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     const int64_t nsc = (int64_t)seg.size() - 1;
     if (ng <= kMaxStreamChunks) {
       if (!h->stream_ctr) {
-        CUDA_TRY(cudaMalloc(&h->stream_ctr, (2 + kMaxStreamChunks) * sizeof(int)));
+        CUDA_TRY(cudaMalloc(&h->stream_ctr, (4 + kMaxStreamChunks + kMaxSegs) * sizeof(int)));
         CUDA_TRY(cudaHostAlloc(&h->stream_flag_host, sizeof(int), cudaHostAllocDefault));
       }
       CUDA_TRY(cudaMemsetAsync(h->stream_ctr, 0, (2 + ng) * sizeof(int), s));

@@ -12,6 +12,20 @@ cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xc
 cudaError_t tc_to_operand_rows(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
                                int64_t L, int D, int64_t prow, cudaStream_t s);
 
+// copy segments of a streamed input: segment j = X rows [end[j-1], end[j])
+constexpr int kMaxSegs = 48;
+struct TcSegTab {
+  int n;
+  int end[kMaxSegs];
+};
+// streaming conversion: one persistent launch (`workers` CTAs + a publisher)
+// following the copy engine (seg_flag[j] == epoch: segment j landed), per-group flags tagged
+// with the call's epoch, *ready = rows converted in order
+bool tc_to_operand_stream_ok(const float* X, int64_t ldx, const float* xcarry, const void* out, int64_t ldo, int D);
+cudaError_t tc_to_operand_stream(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                                 int64_t L, int D, const TcSegTab& segs, const int* seg_flag, int* ready, int* fail,
+                                 int* flags, int* next_group, int epoch, int group, int workers, cudaStream_t s);
+
 // One layer on the tensor-core path.  Wtc: [3*Hpad][Kp] gate-major operand
 // weights; Xop: [L+1][ldop_in] operand input (row 0 = x_{-1}).
 cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, const void* Xop, int64_t ldop_in,

@@ -90,6 +90,193 @@ cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xc
   return tc_to_operand_rows(mode, X, ldx, xcarry, out, ldo, L, D, L + 1, s);
 }
 
+// Streaming conversion (rnnb_forward_host): ONE persistent launch converts
+// the whole sequence while the copy engine is still landing it.  X rows
+// arrive in copy segments (TcSegTab) on two alternating copy streams; a
+// stream write-value after each segment's copy tags seg_flag[j] with the
+// call's epoch.  Groups of `group` rows go round-robin over the worker
+// CTAs (blockIdx >= 1): a worker converts its group as soon as the rows are
+// there (16-byte loads, 8 in flight per thread) and release-stores the call's
+// epoch into flags[g].  CTA 0 is the PUBLISHER: one warp polls 32 group flags
+// at a time and advances *ready = rows converted, the in-order counter the
+// layer kernel's TMA producer waits on.  Workers never wait on each other,
+// so they need not be co-resident (they fill the SMs the layer launch leaves
+// free and whatever register space is left beside its CTAs).
+// History: per-segment conversion launches were latency-bound on the two free
+// SMs (60-90 us per 512-row segment against a 40 us copy); workers
+// publishing the counter themselves in order made every group wait an L2
+// round trip on its predecessor (a 128-hop serial chain).
+// Rows that do not arrive within kStreamTimeoutNs (a profiler serialising
+// the streams) set *fail, release the consumer and end the kernel.
+template <int MODE>
+__global__ void __launch_bounds__(256, 4)
+    to_operand_stream_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ xcarry,
+                             void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow,
+                             const TcSegTab segs, const int* seg_flag, int* ready, int* fail, int* flags,
+                             int* next_group, int epoch, int group) {
+  const int nv = D >> 2;
+  const int ngroups = (int)((L + group - 1) / group);
+  uint64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+  auto timed_out = [&]() {
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    return now - t_start > kStreamTimeoutNs;
+  };
+  if (blockIdx.x == 0) {
+    // ---- publisher ----
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    int base = 0;
+    while (base < ngroups) {
+      int v = 0;
+      if (base + lane < ngroups)
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(flags + base + lane) : "memory");
+      const unsigned m = __ballot_sync(0xffffffffu, v == epoch);
+      const int n = __ffs(~m) - 1;  // leading groups done (m == all ones: __ffs(0) - 1 = -1 -> 32)
+      const int adv = n < 0 ? 32 : n;
+      if (adv > 0) {
+        base += adv;
+        if (base > ngroups) base = ngroups;
+        const int64_t rows = (int64_t)base * group < L ? (int64_t)base * group : L;
+        if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready), "r"((int)rows) : "memory");
+      } else {
+        int f = 0;
+        if (lane == 0) {
+          asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(fail) : "memory");
+          if (!f && timed_out()) {
+            atomicExch(fail, 1);
+            f = 1;
+          }
+        }
+        f = __shfl_sync(0xffffffffu, f, 0);
+        if (f) {  // a worker or this warp gave up: let the consumer run on (the host redoes the call)
+          if (lane == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready), "r"(0x7fffffff) : "memory");
+          return;
+        }
+        __nanosleep(100);
+      }
+    }
+    return;
+  }
+  // ---- workers ----
+  __shared__ int s_fail, s_g;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  auto convert = [&](int64_t r, int v, const float4 x) {  // operand row r, 4 columns from 4v
+    const int d = v << 2;
+    if (MODE == TC_BF16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(x.x, x.y), hi = __floats2bfloat162_rn(x.z, x.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(out) + r * ldo + d) = pk;
+    } else {
+      const float4 h4 = make_float4(round_x(x.x, XR_TF32), round_x(x.y, XR_TF32), round_x(x.z, XR_TF32),
+                                    round_x(x.w, XR_TF32));
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + r * ldo + d) = h4;
+      if (MODE == TC_3XTF32) {
+        const float4 l4 = make_float4(round_x(x.x - h4.x, XR_TF32), round_x(x.y - h4.y, XR_TF32),
+                                      round_x(x.z - h4.z, XR_TF32), round_x(x.w - h4.w, XR_TF32));
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(out) + (r + prow) * ldo + d) = l4;
+      }
+    }
+  };
+  // groups are claimed from a queue, in order: the workers that are resident
+  // convert the next rows to land (a static round-robin would leave holes at
+  // the groups of workers still waiting for an SM, and the in-order counter
+  // would stall on them)
+  while (true) {
+    if (threadIdx.x == 0) s_g = atomicAdd(next_group, 1);
+    __syncthreads();
+    const int g = s_g;
+    if (g >= ngroups) return;
+    const int64_t r0 = (int64_t)g * group, r1 = (r0 + group) < L ? (r0 + group) : L;  // X rows [r0, r1)
+    if (threadIdx.x == 0) {
+      // the copy segment holding the group's last row (the segments land in
+      // order on two alternating copy streams; a segment's write-value tags
+      // its flag with the call's epoch once all of it is in device memory).
+      // A group inside one segment needs only that flag; one that spans two
+      // needs both.
+      int j1 = 0;
+      while (j1 < segs.n - 1 && segs.end[j1] < (int)r1) ++j1;
+      int j0 = j1;
+      while (j0 > 0 && segs.end[j0 - 1] > (int)r0) --j0;
+      for (int j = j0; j <= j1 && !s_fail; ++j) while (true) {
+        int have = 0;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(have) : "l"(seg_flag + j) : "memory");
+        if (have == epoch) break;
+        if (timed_out()) {
+          atomicExch(fail, 1);
+          s_fail = 1;
+          break;
+        }
+        __nanosleep(200);
+      }
+    }
+    __syncthreads();
+    if (s_fail) return;
+    if (g == 0)  // operand row 0 = x_{-1}: the carry or zeros
+      for (int v = threadIdx.x; v < nv; v += blockDim.x)
+        convert(0, v, xcarry ? *reinterpret_cast<const float4*>(xcarry + (v << 2)) : make_float4(0.f, 0.f, 0.f, 0.f));
+    const int n = (int)(r1 - r0) * nv;
+    const int stride = blockDim.x;
+    int i = threadIdx.x;
+    for (; i + 7 * stride < n; i += 8 * stride) {  // 8 independent 16-byte loads in flight per thread
+      float4 x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = i + k * stride, rr = j / nv, v = j - rr * nv;
+        x[k] = __ldcs(reinterpret_cast<const float4*>(X + (r0 + rr) * ldx) + v);
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int j = i + k * stride, rr = j / nv, v = j - rr * nv;
+        convert(r0 + rr + 1, v, x[k]);
+      }
+    }
+    for (; i < n; i += stride) {
+      const int rr = i / nv, v = i - rr * nv;
+      convert(r0 + rr + 1, v, __ldcs(reinterpret_cast<const float4*>(X + (r0 + rr) * ldx) + v));
+    }
+    __syncthreads();  // the CTA's stores happen-before thread 0's release below
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flags + g), "r"(epoch) : "memory");
+  }
+}
+
+bool tc_to_operand_stream_ok(const float* X, int64_t ldx, const float* xcarry, const void* out, int64_t ldo, int D) {
+  // Load the kernels NOW (CUDA loads a kernel's code lazily at its first
+  // launch, and that load waits for the device): the conversion is launched
+  // while the layer kernel is already spinning on its row counter, so a first
+  // launch there stalled until the layer kernel's 2 s time-out.
+  static bool loaded = false;
+  if (!loaded) {
+    cudaFuncAttributes fa;
+    (void)cudaFuncGetAttributes(&fa, to_operand_stream_kernel<TC_BF16>);
+    (void)cudaFuncGetAttributes(&fa, to_operand_stream_kernel<TC_TF32>);
+    (void)cudaFuncGetAttributes(&fa, to_operand_stream_kernel<TC_3XTF32>);
+    loaded = true;
+  }
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  return D % 4 == 0 && ldx % 4 == 0 && ldo % 8 == 0 && al16(X) && (xcarry == nullptr || al16(xcarry)) && al16(out);
+}
+
+cudaError_t tc_to_operand_stream(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
+                                 int64_t L, int D, const TcSegTab& segs, const int* seg_flag, int* ready, int* fail,
+                                 int* flags, int* next_group, int epoch, int group, int workers, cudaStream_t s) {
+  const int grid = workers + 1;  // + the publisher (CTA 0)
+  if (mode == TC_BF16)
+    to_operand_stream_kernel<TC_BF16><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, L + 1, segs, seg_flag, ready, fail,
+                                                           flags, next_group, epoch, group);
+  else if (mode == TC_TF32)
+    to_operand_stream_kernel<TC_TF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, L + 1, segs, seg_flag, ready, fail,
+                                                           flags, next_group, epoch, group);
+  else
+    to_operand_stream_kernel<TC_3XTF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, L + 1, segs, seg_flag, ready,
+                                                             fail, flags, next_group, epoch, group);
+  return cudaGetLastError();
+}
+
 static bool make_map(CUtensorMap* tm, CUtensorMapDataType dt, int es, const void* base, uint64_t inner,
                      uint64_t outer, uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer) {
   EncodeTiledFn enc = encode_tiled();

@@ -70,6 +70,10 @@ struct TcArgs {
   int* h_done;
   int h_gran;
   int* stream_fail;   // set when the input did not arrive in time (see wait_rows)
+  // RNNB_STREAM_TRACE (tuning only): globaltimer stamps, [0] kernel start,
+  // [1 + b] block b's rows seen resident (unit tile 0), [1 + nB + b] block b's
+  // last unit tile stored
+  unsigned long long* trace;
   // 3xTF32 only: items from split_start on (the last, partial wave) are
   // split in two halves on two CTAs (see tc_work); fix holds the first
   // halves' K-chunk sums [slot][3N][128], fixflag their release tags
@@ -317,6 +321,11 @@ __device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n
 // the item's output granule; the host's copy-out stream waits until a
 // granule holds nU x (its blocks) counts.
 __device__ __forceinline__ void tc_count_done(const TcArgs& a, int64_t t0, int et) {
+  if (a.trace && et == 0) {
+    unsigned long long now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    atomicMax(&a.trace[1 + a.nB + (int)(t0 / a.T_b)], now);
+  }
   if (a.h_done == nullptr) return;
   tc_epi_sync();
   if (et == 0) {
@@ -525,6 +534,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __nanosleep(64);
           }
           asm volatile("fence.proxy.async.global;" ::: "memory");  // TMA reads after the acquire
+          if (a.trace && u == 0 && w.part != 1) {
+            unsigned long long now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            a.trace[1 + b] = now;
+            if (item == 0) a.trace[0] = t_start;
+          }
         }
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % C::STAGES;

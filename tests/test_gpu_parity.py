@@ -591,6 +591,30 @@ def test_host_streaming_tensor_core_matches_device(P, oracle, kind, mode, d, L, 
     st.close()
 
 
+@pytest.mark.parametrize("kind,mode,d,L,T", [("qrnn", "f32", 1024, 2048, 32), ("sru", "f32", 512, 777, 16),
+                                             ("qrnn", "bf16", 1024, 3000, 64), ("sru", "tf32", 640, 5000, 32)])
+def test_host_streaming_pinned_buffers_zero_copy_output(P, oracle, kind, mode, d, L, T, monkeypatch):
+    """rnnb_forward_host with PINNED host buffers (what bench.py's e2e leg
+    passes): the persistent conversion kernel follows the copy segments and the
+    layer epilogue stores h straight into the caller's pinned buffer (no
+    copy-out) -- bitwise the device call, repeatably, with the zero-copy
+    output switched off too."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 1, 91, np.float32)
+    X = np.random.default_rng(30).standard_normal((L, d)).astype(np.float32)
+    st = P.DeviceStack(kind, layers, mode=mode)
+    ref = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
+    assert st.query(9) == 1
+    Xp = torch.from_numpy(X).pin_memory()
+    Hp = torch.full((L, d), float("nan"), dtype=torch.float32).pin_memory()
+    for zc in ("1", "0", "1"):
+        monkeypatch.setenv("RNNB_ZC_OUT", zc)
+        Hp.fill_(float("nan"))
+        st.forward_host(Xp.numpy(), T, out=Hp.numpy())
+        assert Hp.numpy().tobytes() == ref.tobytes()
+    st.close()
+
+
 @pytest.mark.parametrize("kind,d,L", [("qrnn", 1024, 2048), ("sru", 1024, 3000), ("qrnn", 2048, 700)])
 def test_split_last_wave_is_bitwise_neutral(P, oracle, kind, d, L, monkeypatch):
     """3xTF32: the last partial wave's items run as two K halves on two CTAs

@@ -49,3 +49,11 @@ if os.environ.get("E2E_TIMELINE"):
     print(f"wall {(t1 - t0) * 1e6:.1f} us; device span {max(e.time_range.end for e in evs) - base:.1f} us")
     for e in sorted(evs, key=lambda e: e.time_range.start):
         print(f"  {e.time_range.start - base:9.1f} .. {e.time_range.end - base:9.1f}  {e.name[:60]}")
+
+if os.environ.get("E2E_TRACE"):
+    # device-side event trace of the streaming path (RNNB_STREAM_TRACE, rnnb_api.cu)
+    os.environ["RNNB_STREAM_TRACE"] = "1"
+    for _ in range(2):
+        t0 = time.perf_counter()
+        st.forward_host(Xn, a.block, out=Hn)
+        print(f"traced call wall {(time.perf_counter() - t0) * 1e6:.1f} us", flush=True)
