@@ -176,6 +176,37 @@ __device__ __forceinline__ void tc_issue_ktile(uint32_t d0, uint64_t a0, uint64_
         "setp.ne.b32 p, %4, 0;\n\t" RNNB_X3GATE(0) RNNB_X3GATE(1) RNNB_X3GATE(2) "}\n" ::"r"(d0),
         "l"(a0), "l"(b0), "r"(idesc), "r"(acc), "l"(lo16), "r"(idesc_n), "r"(2 * n));
 }
+// One 3xTF32 k-tile on the fine-grained ring as ONE asm block: the three
+// gates' W slots are consecutive (32 KB = 2048 sixteen-byte units apart, W_lo
+// 16 KB after W_hi), and each gate's slot is RELEASED by its own commit right
+// after its 8 MMAs (empty barriers 8 B apart), the x slot after the last
+// gate.  Per gate: 4 K-steps x (W_hi . [x_hi | x_lo] into [d, d+2N), then
+// W_lo . x_hi into [d+N, d+2N)).  One block per k-tile, not per gate: every
+// asm block costs ptxas ~60 uniform-datapath instructions of operand set-up
+// that the tensor pipe's short queue does not hide (per-gate blocks: MMA-only
+// time 151 -> 189 us on cfg2).
+#define RNNB_G3STEP(ACCP)                                                   \
+  "@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, b, %3, " ACCP ";\n\t"     \
+  "add.s64 al, a, 1024;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [dc], al, b, %6, 1;\n\t"
+#define RNNB_G3NEXT "add.s64 a, a, 2;\n\tadd.s64 b, b, 2;\n\t" RNNB_G3STEP("1")
+#define RNNB_G3GATE(G)                                                                               \
+  "add.s64 a, %1, " #G "*2048;\n\tmov.b64 b, %2;\n\tmad.lo.s32 d, %8, " #G ", %0;\n\tadd.s32 dc, d, %5;\n\t" \
+  RNNB_G3STEP("p") RNNB_G3NEXT RNNB_G3NEXT RNNB_G3NEXT                                               \
+  "add.s32 eb, %7, " #G "*8;\n\t"                                                                    \
+  "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [eb];\n\t"
+__device__ __forceinline__ void tc_issue_ktile_x3_fine(uint32_t d0, uint64_t a0, uint64_t b0, uint32_t idesc_2n,
+                                                       uint32_t acc, uint32_t n, uint32_t idesc_n, uint32_t emptyw0,
+                                                       uint32_t gcols, uint32_t emptyx) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 a, b, al;\n\t.reg .b32 d, dc, eb;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" RNNB_G3GATE(0) RNNB_G3GATE(1) RNNB_G3GATE(2)
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%9];\n\t}\n" ::"r"(d0),
+      "l"(a0), "l"(b0), "r"(idesc_2n), "r"(acc), "r"(n), "r"(idesc_n), "r"(emptyw0), "r"(gcols), "r"(emptyx)
+      : "memory");
+}
+#undef RNNB_G3STEP
+#undef RNNB_G3NEXT
+#undef RNNB_G3GATE
 #undef RNNB_MMA
 #undef RNNB_KSTEP
 #undef RNNB_GATE
@@ -432,7 +463,24 @@ struct TcCfg {
   static constexpr int TMEM_COLS = (USED_COLS <= 32) ? 32 : (USED_COLS <= 64) ? 64
                                    : (USED_COLS <= 128) ? 128 : (USED_COLS <= 256) ? 256 : 512;
   static_assert(USED_COLS <= 512, "TMEM holds 512 columns");
-  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  // 3xTF32: FINE-grained ring.  A 104 KB stage (both planes of a k-tile) left
+  // room for two stages only, and a stage is refilled only after ALL its 24
+  // MMAs: half the buffer was idle while the other half was read, and the
+  // L2 feed (which, like the MMA issue, needs ~0.65 us per k-tile) could not
+  // overlap it (loads + MMAs 199 us vs 152 us for either alone on cfg2).  Now
+  // a W slot holds one gate's hi + lo tiles (32 KB, freed after that gate's 8
+  // MMAs) and the x tiles ([x_hi ; x_lo], shared by the three gates) have
+  // their own small ring.
+  static constexpr bool FINE = CHUNKED;
+  static constexpr int W_SLOT = 2 * A_BYTES;
+  static constexpr int X_SLOT = SPLIT * B_BYTES;
+  static constexpr int NW = 6;
+  static constexpr int NX = (227 * 1024 - 2048 - NW * W_SLOT) / X_SLOT < 4 ? (227 * 1024 - 2048 - NW * W_SLOT) / X_SLOT : 4;
+  static_assert(!FINE || NX >= 2, "x ring too small");
+  static constexpr int RING_BYTES = FINE ? NW * W_SLOT + NX * X_SLOT : STAGES * STAGE_BYTES;
+  static constexpr int NFULL = FINE ? NW + NX : STAGES;  // full barriers (then as many empty ones)
+  static constexpr size_t SMEM = (size_t)RING_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(2 * NFULL * 8 + 64 + 8 <= 256, "barrier area");
 };
 
 // This CTA's k-th unit of work.  Whole items blockIdx.x + k*grid below
@@ -469,9 +517,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   using C = TcCfg<MODE, N>;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + (size_t)C::STAGES * C::STAGE_BYTES);
-  uint64_t* empty = full + C::STAGES;
-  uint64_t* acc_full = empty + C::STAGES;
+  // FINE: full = [W slots | x slots], empty likewise
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + (size_t)C::RING_BYTES);
+  uint64_t* empty = full + C::NFULL;
+  uint64_t* acc_full = empty + C::NFULL;
   uint64_t* acc_empty = acc_full + 4;
   uint32_t* tmem_base_smem = reinterpret_cast<uint32_t*>(acc_empty + 4);
 
@@ -479,7 +528,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int nitems = a.nU * a.nB;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < C::STAGES; ++s) {
+    for (int s = 0; s < C::NFULL; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
@@ -541,6 +590,42 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (item == 0) a.trace[0] = t_start;
           }
         }
+        if constexpr (C::FINE) {
+          // ONE full barrier per k-tile (ring of two: k-tile parity) counts the
+          // bytes of its x slot and its three W slots -- the MMA warp waits
+          // once per k-tile (four waits per k-tile left the tensor pipe's
+          // short queue dry: MMA-only time 151 -> 182 us); the slots are
+          // still loaded one by one, as soon as each is released
+          for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
+            const int tap = kt >= a.nKtap ? 1 : 0;
+            const int kx = (kt - tap * a.nKtap) * C::KT;
+            const int xs = it % C::NX;
+            uint64_t* fk = &full[it & 1];
+            mbar_wait(&empty[C::NW + xs], ((it / C::NX) & 1) ^ 1);
+            // the k-tile's first W slot is free only after the MMA warp has
+            // passed this barrier's previous phase (k-tile it-2): arm it after
+            // that wait, never twice in one phase
+            mbar_wait(&empty[(it & 1) * 3], ((it >> 1) & 1) ^ 1);
+            unsigned char* xt = tsm + C::NW * C::W_SLOT + (size_t)xs * C::X_SLOT;
+            if (!(a.dbg & 128)) {
+              mbar_arrive_expect_tx(fk, C::X_SLOT + 3 * C::W_SLOT);
+#pragma unroll
+              for (int p = 0; p < C::SPLIT; ++p)
+                tma_load_2d(xt + p * C::B_BYTES, &tmX, kx, (int)(p * (a.L + 1)) + t0 + 1 - tap, fk);
+            }
+            for (int g = 0; g < 3; ++g) {
+              const int ws = (it & 1) * 3 + g;
+              if (g > 0) mbar_wait(&empty[ws], ((it >> 1) & 1) ^ 1);
+              unsigned char* wt = tsm + (size_t)ws * C::W_SLOT;
+              if (a.dbg & 128) continue;
+#pragma unroll
+              for (int p = 0; p < C::SPLIT; ++p)
+                tma_load_2d(wt + p * C::A_BYTES, &tmW, kt * C::KT, (p * 3 + g) * a.Hpad + u * 128, fk);
+            }
+            if (a.dbg & 128) mbar_arrive(fk);  // timing experiment: no loads
+          }
+          continue;
+        }
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
           const int s = it % C::STAGES;
           // plain try_wait (the instruction suspends in hardware): a
@@ -590,6 +675,40 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             dbase = tmem + ab * C::ACC_COLS;
             mbar_wait(&acc_empty[ab], ((acc_it / C::NACC) & 1) ^ 1);
             tc_fence_after();
+          }
+          if constexpr (C::FINE) {
+            static_assert(C::NW == 6, "a k-tile's three W slots are consecutive: slots {0,1,2} / {3,4,5}");
+            const int xs = it % C::NX;
+            const int wb = (it & 1) * 3;  // first W slot of this k-tile
+            const uint32_t wph = (it >> 1) & 1;
+            mbar_wait(&full[it & 1], wph);
+            tc_fence_after();
+            if (a.dbg & 2048) {  // timing experiment: the old coarse issue block + software arrives (no per-gate commits)
+              tc_issue_ktile<MODE>(dbase, sw128_desc(tsm + (size_t)wb * C::W_SLOT),
+                                   sw128_desc(tsm + C::NW * C::W_SLOT + (size_t)xs * C::X_SLOT), idesc_2n, kc != 0, N,
+                                   idesc_n, (uint64_t)(C::A_BYTES >> 4));
+              if (lane == 0) {
+                mbar_arrive(&empty[wb]);
+                mbar_arrive(&empty[wb + 1]);
+                mbar_arrive(&empty[wb + 2]);
+              }
+              __syncwarp();
+              tc_commit_elect(&empty[C::NW + xs]);
+            } else if (!(a.dbg & 64)) {
+              tc_issue_ktile_x3_fine(dbase, sw128_desc(tsm + (size_t)wb * C::W_SLOT),
+                                     sw128_desc(tsm + C::NW * C::W_SLOT + (size_t)xs * C::X_SLOT), idesc_2n, kc != 0, N,
+                                     idesc_n, smem_u32(&empty[wb]), C::GCOLS, smem_u32(&empty[C::NW + xs]));
+            } else {
+              tc_commit_elect(&empty[wb]);
+              tc_commit_elect(&empty[wb + 1]);
+              tc_commit_elect(&empty[wb + 2]);
+              tc_commit_elect(&empty[C::NW + xs]);
+            }
+            if (kc == C::CK - 1 || kt == w.kt1 - 1) {
+              tc_commit_elect(&acc_full[ab]);  // this K-chunk's partial products complete
+              ++acc_it;
+            }
+            continue;
           }
           const int s = it % C::STAGES;
           mbar_wait(&full[s], (it / C::STAGES) & 1);
