@@ -228,15 +228,18 @@ bool use_tc(const rnnb_stack* h, int64_t Tb) {
   // live in registers: N <= 32), i.e. each weight is read into the tensor
   // pipe once per 32 steps -- the same cap as the FFMA kernel's 32-column
   // passes (cfg2 T_b=64: 2.9 M steps/s on the FFMA fallback before)
-  if (h->mode == RNNB_F32X3) return Tb >= 16;
+  if (h->mode == RNNB_F32X3) return Tb >= 8;
   // fp32 (the reference precision): the same fp32-accurate 3xTF32 tcgen05
-  // path from T_b = 16 on (normwise error 1e-6 .. 6e-6 against the oracle on
+  // path from T_b = 8 on (N = 16 accumulator columns, half of them masked:
+  // cfg2 3.04 vs 2.65 M steps/s on the FFMA kernel, cfg3 0.97 vs 0.65 M; at
+  // T_b = 4 the FFMA kernel wins 2.18 vs 1.54 M; RNNB_F32_TC_MIN) (normwise error 1e-6 .. 6e-6 against the oracle on
   // the BASELINE shapes, inside the 1e-5 bound: tests/test_gpu_full_shapes.py;
   // 2.5x the FFMA kernel at cfg2 T_b = 32).  RNNB_F32_TC=0 keeps every T_b
   // on the FFMA kernels (bitwise invariant to how calls chunk the sequence).
   if (h->mode == RNNB_F32) {
     const char* e = getenv("RNNB_F32_TC");
-    return !(e && e[0] == '0') && Tb >= 16;
+    const char* m = getenv("RNNB_F32_TC_MIN");
+    return !(e && e[0] == '0') && Tb >= (m ? atoi(m) : 8);
   }
   return false;
 }
@@ -929,6 +932,12 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     const int64_t nsc = (int64_t)seg.size() - 1;
     int64_t ldop = 0;
     if ((st = ensure_tc_op(h, 0, L, &ldop)) != RNNB_OK) return st;
+    // everything that may wait for the device (scratch (re)allocation, the
+    // lazy load of the layer kernel's code) happens HERE, before the
+    // conversion kernel starts spinning on rows the host has yet to enqueue
+    const int64_t nBt = (L + Tb - 1) / Tb;
+    CUDA_TRY(tc_layer_preload(h->kind, mode, (int)Tb));
+    if ((st = tc_layer_scratch(h, h->layers[0], nBt, nU, tc_pick_n((int)Tb), mode == TC_3XTF32, s)) != RNNB_OK) return st;
     const size_t opes = mode == TC_BF16 ? 2 : 4;
     if (!h->stream_ctr) {
       CUDA_TRY(cudaMalloc(&h->stream_ctr, (4 + kMaxStreamChunks + kMaxSegs) * sizeof(int)));
@@ -983,7 +992,6 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       tname.push_back(name);
     };
     mark(s, "start");
-    const int64_t nBt = (L + Tb - 1) / Tb;
     if (trace) {
       if (h->stream_trace) cudaFree(h->stream_trace);
       CUDA_TRY(cudaMalloc(&h->stream_trace, (1 + 2 * nBt) * sizeof(unsigned long long)));
@@ -1050,22 +1058,11 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     // copy engine starts at once and stays busy while the host encodes and
     // launches the kernel, which waits on the row counter anyway), the rest
     // after it
-    const char* env_p = getenv("RNNB_STREAM_PRE");
-    const int64_t want_pre = env_p ? atoll(env_p) : 3;
-    const int64_t pre = nsc < want_pre ? nsc : want_pre;
-    for (int64_t i = 0; i < pre; ++i)
-      if ((st = copy_in(i)) != RNNB_OK) return st;
-    h->stream_ready = h->stream_ctr;
-    h->stream_done = dHz ? nullptr : h->stream_ctr + 2;
-    h->stream_chunk = (int)g;
-    mark(s, "before layer kernel");
-    st = rnnb_forward(h, dX, din, L, block_size, dHz ? dHz : dH, dh, dC, dXC, stream);
-    mark(s, "layer kernel done");
-    // the persistent conversion goes AFTER the layer launch: rnnb_forward may
-    // (re)allocate scratch, and cudaMalloc / cudaFree wait for the device --
-    // a conversion kernel already spinning on rows the host has not enqueued
-    // yet would hold that wait until its time-out
-    if (st == RNNB_OK && conv_stream) {
+    // the persistent conversion kernel (everything that could wait for the
+    // device was done above, so it may be launched on either side of the layer
+    // kernel without a first-use stall)
+    auto launch_conv = [&]() -> rnnb_status {
+      if (!conv_stream) return RNNB_OK;
       const char* env_g = getenv("RNNB_STREAM_GROUP");
       int group = env_g ? atoi(env_g) : 16;
       if (group < 1) group = 16;
@@ -1074,13 +1071,39 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       if (workers < 1) workers = 1;
       CUDA_TRY(tc_to_operand_stream(mode, fX, din, h->kind == RNNB_QRNN ? fXC : nullptr, h->op, ldop, L, (int)din,
                                     segtab, seg_flag, h->stream_ctr, h->stream_ctr + 1, h->stream_flags, copied_ctr + 1,
-                                    h->stream_epoch,
-                                    group, workers, h->s_cv));
+                                    h->stream_epoch, group, workers, h->s_cv));
       mark(h->s_cv, "conversion kernel done");
+      return RNNB_OK;
+    };
+    const char* env_p = getenv("RNNB_STREAM_PRE");
+    int64_t want_pre = env_p ? atoll(env_p) : 3;
+    if (want_pre < 1) want_pre = 1;
+    const int64_t pre = nsc < want_pre ? nsc : want_pre;
+    // the conversion kernel goes behind the layer launch: launched first, its
+    // workers spread over idle SMs and the layer CTAs that land beside them run
+    // slower (e2e 0.50-0.55 ms vs 0.39-0.44 ms); RNNB_STREAM_CONV_FIRST=1 for A/B
+    const bool conv_first = getenv("RNNB_STREAM_CONV_FIRST") != nullptr;
+    for (int64_t i = 0; i < pre; ++i) {
+      if ((st = copy_in(i)) != RNNB_OK) return st;
+      if (i == 0 && conv_first && (st = launch_conv()) != RNNB_OK) return st;
     }
+    h->stream_ready = h->stream_ctr;
+    h->stream_done = dHz ? nullptr : h->stream_ctr + 2;
+    h->stream_chunk = (int)g;
+    mark(s, "before layer kernel");
+    st = rnnb_forward(h, dX, din, L, block_size, dHz ? dHz : dH, dh, dC, dXC, stream);
+    mark(s, "layer kernel done");
+    if (st == RNNB_OK && !conv_first && (st = launch_conv()) != RNNB_OK) return st;
     h->stream_ready = nullptr;
     h->stream_done = nullptr;
-    if (st != RNNB_OK) return st;
+    if (st != RNNB_OK) {
+      // the conversion kernel may already be waiting for the remaining rows: let it finish
+      if (conv_first && conv_stream) {
+        for (int64_t i = pre; i < nsc; ++i) (void)copy_in(i);
+        (void)cudaStreamSynchronize(h->s_cv);
+      }
+      return st;
+    }
     for (int64_t i = pre; i < nsc; ++i)
       if ((st = copy_in(i)) != RNNB_OK) return st;
     int64_t launches = h->last_launches + nsc;  // + the per-segment operand conversions

@@ -31,6 +31,9 @@ cudaError_t tc_to_operand_stream(int mode, const float* X, int64_t ldx, const fl
 cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, const void* Xop, int64_t ldop_in,
                          int num_sms, cudaStream_t s, int* grid_out);
 
+// load one layer-kernel variant without launching it (see launch_tc)
+cudaError_t tc_layer_preload(int cell, int mode, int T_b);
+
 int tc_pick_n(int T_b);
 int tc_max_n(int mode);
 

@@ -290,6 +290,9 @@ static bool make_map(CUtensorMap* tm, CUtensorMapDataType dt, int es, const void
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// grid == 0: only load the kernel and set its attribute (CUDA loads kernel code
+// lazily at the first launch, and that load waits for the device -- fatal for
+// a first launch made while another kernel spins on this one's progress)
 template <int CELL, int MODE, int N>
 static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx, int grid,
                              cudaStream_t s) {
@@ -301,6 +304,7 @@ static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUten
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  if (grid == 0) return cudaSuccess;
   // programmatic dependent launch: the CTAs set up (barriers, TMEM, tensor-map
   // prefetch) while the preceding kernel -- usually the operand conversion --
   // drains, then wait on griddepcontrol before touching global memory
@@ -316,6 +320,8 @@ static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUten
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k, a, tw, tx);
 }
+
+cudaError_t tc_layer_preload(int cell, int mode, int T_b);
 
 int tc_max_n(int mode) { return mode == TC_3XTF32 ? 32 : 128; }
 
@@ -372,6 +378,25 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
   if (mode == TC_BF16) return run_n<QRNN, TC_BF16>(N, a, tw, tx, grid, s);
   if (mode == TC_TF32) return run_n<QRNN, TC_TF32>(N, a, tw, tx, grid, s);
   return run_n<QRNN, TC_3XTF32>(N, a, tw, tx, grid, s);
+}
+
+cudaError_t tc_layer_preload(int cell, int mode, int T_b) {
+  const int N = tc_pick_n(T_b);
+  const TcArgs a{};
+  const CUtensorMap tm{};
+  if (cell == LINEAR) {
+    if (mode == TC_BF16) return run_n<LINEAR, TC_BF16>(N, a, tm, tm, 0, nullptr);
+    if (mode == TC_TF32) return run_n<LINEAR, TC_TF32>(N, a, tm, tm, 0, nullptr);
+    return cudaErrorInvalidValue;
+  }
+  if (cell == SRU) {
+    if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tm, tm, 0, nullptr);
+    if (mode == TC_TF32) return run_n<SRU, TC_TF32>(N, a, tm, tm, 0, nullptr);
+    return run_n<SRU, TC_3XTF32>(N, a, tm, tm, 0, nullptr);
+  }
+  if (mode == TC_BF16) return run_n<QRNN, TC_BF16>(N, a, tm, tm, 0, nullptr);
+  if (mode == TC_TF32) return run_n<QRNN, TC_TF32>(N, a, tm, tm, 0, nullptr);
+  return run_n<QRNN, TC_3XTF32>(N, a, tm, tm, 0, nullptr);
 }
 
 }  // namespace rnnb

@@ -148,7 +148,7 @@ def test_baseline_cfg2_full(P, oracle, f32_tc, monkeypatch):
     """BASELINE cfg2 (QRNN 1024, L=2048) at full size: reference row
     subsample + c_T, plus the oracle over the whole output at every T_b --
     on the FFMA kernels (RNNB_F32_TC=0) and on fp32 mode's default dispatch
-    (3xTF32 tcgen05 from T_b = 16)."""
+    (3xTF32 tcgen05 from T_b = 8)."""
     import torch
     monkeypatch.setenv("RNNB_F32_TC", f32_tc)
     from paper_1803_11389_b200 import workloads
@@ -163,7 +163,7 @@ def test_baseline_cfg2_full(P, oracle, f32_tc, monkeypatch):
         if T == 32:
             assert_f32(H[g["cfg2_T32_rows"]], g["cfg2_T32_Hrows"])
             assert_f32(c.cpu().numpy(), g["cfg2_T32_c"])
-        if f32_tc == "0" or T < 16:
+        if f32_tc == "0" or T < 8:
             assert st.query(3) == 1 and st.query(6) == 1  # SMEM-resident, warp-specialised FFMA
         else:
             assert st.query(9) == 1  # 3xTF32 on tcgen05
@@ -455,6 +455,7 @@ def test_register_resident_kernel(P, oracle, kind, d, monkeypatch):
     layers = oracle.generate_layers(kind, d, d, 2, 57, np.float32)
     X = torch.from_numpy(np.random.default_rng(14).standard_normal((333, d)).astype(np.float32)).cuda()
     st = P.DeviceStack(kind, layers)
+    monkeypatch.setenv("RNNB_F32_TC", "0")  # the FFMA kernels (fp32 mode runs T_b >= 8 on tcgen05 by default)
     for T in (1, 2, 3, 8):
         monkeypatch.setenv("RNNB_REG", "1")
         H = st.forward(X, T).cpu().numpy()
