@@ -147,7 +147,8 @@ def tc_pick_n(T):
     return 16 if T <= 16 else 32 if T <= 32 else 64 if T <= 64 else 128
 
 
-def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc=None, sm_mhz=None, nt=None):
+def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc=None, sm_mhz=None, nt=None,
+                 reg=False):
     """Roofline of the dominant kernel, per regime:
 
     * tcgen05 path (bf16 / tf32 / fp32-accurate 3xTF32): the weights are
@@ -195,7 +196,8 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
         n_instr /= launches_per_step
         l2_bytes /= launches_per_step
         t_mma = n_instr * cyc / 148 / (mhz * 1e6)
-        l2 = (_json("l2_peak.json") or {}).get("l2_read_gbs", 23887.0)
+        l2j = _json("l2_peak.json") or {}
+        l2 = max(l2j.get("l2_read_gbs", 23887.0), l2j.get("l2_tma_tile_gbs_in_kernel", 0.0))
         t_l2 = l2_bytes / (l2 * 1e9)
         t_bound = max(t_mma, t_l2)
         nominal = pk["bf16_tflops"] * (1.0 if mode == "bf16" else 0.5)
@@ -220,9 +222,35 @@ def roofline_for(w, T_b, mode, ms_per_launch, launches_per_step, pk, traffic, tc
     if mode == "f64":
         peak *= 0.5
         src += " x 0.5 (fp64 rate)"
-    out.update({"bound": "compute", "pipe": "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)",
-                "achieved": round(achieved, 3), "peak": round(peak, 2), "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "peak_source": src})
+    # FFMA kernels keep a layer's weights in shared memory and read each weight
+    # once per pass of min(T_b, 32) time steps: at small T_b the applicable
+    # bound is that SHARED-MEMORY weight stream (north_star's "weight bandwidth
+    # for small T_b"), not the FMA pipe.  Peak: tools/lds_bench.cu, 16-byte
+    # loads at 1.067 cycles per warp and scheduler = 120 B/clk/SM.
+    lds = _json("lds_bench_r1.json")
+    lds_bpc = 120.0
+    if lds:
+        best = min(r["clk_per_warp_lds"] for r in lds["rows"] if r["bytes"] == 16)
+        lds_bpc = 512.0 / (4.0 * best)
+    smem_gbs = 148 * lds_bpc * mhz * 1e6 / 1e9
+    t_pass = min(T_b, 32)
+    smem_bytes = params * s_w * -(-L // t_pass) / launches_per_step
+    t_smem = 0.0 if reg else smem_bytes / (smem_gbs * 1e9)  # ffma_reg: the weights live in registers
+    t_fma = flops / (peak * 1e12)
+    t_bound = max(t_smem, t_fma)
+    smem_bound = t_smem > t_fma
+    out.update({"bound": "smem" if smem_bound else "compute",
+                "pipe": ("shared-memory weight stream (weights resident in SMEM, read once per block)" if smem_bound
+                         else "fp64 dfma (CUDA cores)" if mode == "f64" else "fp32 ffma (CUDA cores)"),
+                "achieved": round(achieved, 3), "peak": round(flops / t_bound / 1e12, 2), "unit": "TFLOP/s",
+                "frac": round(t_bound / sec, 4),
+                "peak_source": (f"max(FMA pipe {peak:.1f} TFLOP/s [{src}] = {t_fma * 1e6:.1f} us, shared-memory weight "
+                                f"stream {smem_bytes / 1e9:.3g} GB / {smem_gbs:.0f} GB/s [tools/lds_bench.cu: "
+                                f"{lds_bpc:.0f} B/clk/SM] = {t_smem * 1e6:.1f} us)"),
+                "fma_pipe": {"peak_tflops": round(peak, 2), "frac": round(achieved / peak, 4)},
+                "smem_weight_stream": {"bytes": smem_bytes, "peak_gbs": round(smem_gbs, 1),
+                                       "achieved_gbs": round(smem_bytes / sec / 1e9, 1),
+                                       "frac": round(t_smem / sec, 4)}})
     sw = _json("ncu_sweep_r1.json")
     if sw and w.name == "cfg2" and mode in ("f32", "f32_ffma"):
         for r in sw["rows"]:
@@ -364,7 +392,7 @@ def time_configs(args, local_rank, pk, mhz):
                 ev[i][1].record()
             torch.cuda.synchronize()
             ms = sum(a.elapsed_time(b) for a, b in ev) / steps
-            rf = roofline_for(w, T, mode, ms, 1, pk, None, tc=all(tc), sm_mhz=mhz)
+            rf = roofline_for(w, T, mode, ms, 1, pk, None, tc=all(tc), sm_mhz=mhz, reg=all(reg))
             kern = ("tc_layer (tcgen05)" if all(tc) else "ffma_reg (register-resident)" if all(reg)
                     else "ffma_ws weight-streaming" if all(wst) else "ffma_ws (SMEM-resident)" if all(wsk)
                     else "ffma_layer")
@@ -483,7 +511,7 @@ def run_ours(args, rank, world, local_rank):
         out_ = {}
         for T_b, r in res.items():
             rf = roofline_for(w, T_b, mode, r["ms_per_step"] / (r["launches"] or 1), r["launches"] or 1,
-                              pk, None, tc=all(r["tcgen05"]), sm_mhz=mhz)
+                              pk, None, tc=all(r["tcgen05"]), sm_mhz=mhz, reg=all(r.get("ffma_reg", [False])))
             row = {"steps_per_s": round(L * world / (r["ms_per_step"] / 1e3), 1),
                    "ms_per_step": round(r["ms_per_step"], 5), "frac": rf["frac"], "bound": rf["bound"],
                    "tflops": rf["achieved"], "peak_tflops": rf["peak"], "pipe": rf["pipe"],
@@ -498,7 +526,7 @@ def run_ours(args, rank, world, local_rank):
 
     roof = roofline_for(w, args.block, args.mode, head["ms_per_step"] / (head["launches"] or 1),
                         head["launches"] or 1, pk, load_traffic(args.workload, args.block, args.mode),
-                        tc=all(head["tcgen05"]), sm_mhz=mhz)
+                        tc=all(head["tcgen05"]), sm_mhz=mhz, reg=all(head.get("ffma_reg", [False])))
     roof["peaks_file"] = pk_src
     resident = [bool(st.query(3, li)) for li in range(st.n_layers)]
     line = {
