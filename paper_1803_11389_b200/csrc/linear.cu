@@ -182,6 +182,31 @@ rnnb_status linear_set(rnnb_linear* h, const void* W, const void* bias, int src_
       LCUDA_TRY(cudaMemcpy(h->bias_f, bf.data(), bf.size() * 4, cudaMemcpyHostToDevice));
     }
   } else {
+    if (h->mode == RNNB_F32) {
+      // + tf32 hi / lo planes for the fp32-accurate 3xTF32 tensor-core path
+      // (layers whose items fill the GPU; linear_forward)
+      const int KT = 32;
+      const int64_t Dtc = (h->din + KT - 1) / KT * KT;
+      h->Hpad = (int)(((h->dout + 2) / 3 + 127) / 128 * 128);
+      h->tcKp = (int)Dtc;
+      const size_t rows = (size_t)3 * h->Hpad;
+      std::vector<float> tc(2 * rows * Dtc, 0.f);
+      for (int64_t r = 0; r < h->dout; ++r)
+        for (int64_t k = 0; k < h->din; ++k) {
+          const float v = (float)get(W, r * h->din + k);
+          const float hi = tf32_rna(v);
+          tc[(size_t)r * Dtc + k] = hi;
+          tc[(rows + (size_t)r) * Dtc + k] = tf32_rna(v - hi);
+        }
+      LCUDA_TRY(cudaMalloc(&h->Wtc, tc.size() * 4));
+      LCUDA_TRY(cudaMemcpy(h->Wtc, tc.data(), tc.size() * 4, cudaMemcpyHostToDevice));
+      if (bias) {
+        std::vector<float> bf((size_t)h->dout);
+        for (int64_t r = 0; r < h->dout; ++r) bf[(size_t)r] = (float)get(bias, r);
+        LCUDA_TRY(cudaMalloc(&h->bias_f, bf.size() * 4));
+        LCUDA_TRY(cudaMemcpy(h->bias_f, bf.data(), bf.size() * 4, cudaMemcpyHostToDevice));
+      }
+    }
     const size_t es = h->mode == RNNB_F64 ? 8 : 4;
     std::vector<unsigned char> w((size_t)n * es);
     for (int64_t i = 0; i < n; ++i) {
@@ -216,11 +241,19 @@ rnnb_status linear_forward(rnnb_linear* h, const void* X, int64_t ldx, int64_t L
   LCUDA_TRY(dg.err);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   h->launches = 0;
-  if (tensor_mode(h->mode)) {
-    const int mode = h->mode == RNNB_BF16 ? TC_BF16 : TC_TF32;
+  // fp32: the 3xTF32 tcgen05 path when its (128-column plane triple, 32-row
+  // block) items fill the GPU (cfg3's projection and logits), else the FFMA GEMM
+  bool x3 = false;
+  if (h->mode == RNNB_F32 && h->Wtc != nullptr) {
+    const char* e = getenv("RNNB_F32_TC");
+    const int64_t items = (int64_t)(h->Hpad / 128) * ((L + 31) / 32);
+    x3 = !(e && e[0] == '0') && getenv("RNNB_NO_TC") == nullptr && items >= h->num_sms;
+  }
+  if (tensor_mode(h->mode) || x3) {
+    const int mode = x3 ? TC_3XTF32 : h->mode == RNNB_BF16 ? TC_BF16 : TC_TF32;
     const int es = mode == TC_BF16 ? 2 : 4;
     const int64_t ldop = (h->din + 7) / 8 * 8;
-    const size_t opb = (size_t)(L + 1) * ldop * es;
+    const size_t opb = (size_t)(x3 ? 2 : 1) * (L + 1) * ldop * es;
     if (h->op_bytes < opb) {
       if (h->op) cudaFree(h->op);
       h->op = nullptr;
@@ -234,7 +267,8 @@ rnnb_status linear_forward(rnnb_linear* h, const void* X, int64_t ldx, int64_t L
     a.ldh = ldy;
     a.bias = h->bias_f;
     a.L = L;
-    a.T_b = 64;  // N = 64: double-buffered TMEM accumulators, epilogue overlaps the next item's MMAs
+    a.T_b = x3 ? 32 : 64;  // N = 64: double-buffered TMEM accumulators, epilogue overlaps the next item's MMAs
+                           // (3xTF32 keeps its chunk partials in registers: N = 32)
     a.H = (int)h->dout;
     a.Hpad = h->Hpad;
     a.D = (int)h->din;

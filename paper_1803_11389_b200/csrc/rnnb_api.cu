@@ -1,5 +1,6 @@
 // C ABI of the blocked SRU/QRNN path (see include/rnnb.h).
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -910,6 +911,7 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
   const bool want_tc_stream = !h->stream_disabled.load() && !(env_s && env_s[0] == '0') && h->n_layers == 1 &&
                               use_tc_layer(h, h->layers[0], L, T) && h->num_sms > 8;
   if (want_tc_stream && so.write && so.wait) {
+    const auto t_call = std::chrono::steady_clock::now();
     const int mode = tc_mode_of(h->mode);
     const int64_t Tb = tc_block(h, T);
     const Layer& ly = h->layers[0];
@@ -1125,9 +1127,17 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
     CUDA_TRY(cudaEventRecord(ev_done, h->s_in2));
     CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
-    CUDA_TRY(cudaMemcpyAsync(h->stream_flag_host, h->stream_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
     mark(s, "all done");
     CUDA_TRY(cudaStreamSynchronize(s));
+    // The time-out flag is set only by a kernel thread that waited
+    // kStreamTimeoutNs (2 s) for rows: a call that returned sooner cannot have
+    // failed, and skips the flag's copy-out (a copy-engine round trip behind
+    // the layer kernel on every call).
+    *h->stream_flag_host = 0;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t_call).count() > 1.0) {
+      CUDA_TRY(cudaMemcpyAsync(h->stream_flag_host, h->stream_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+    }
     if (trace) {
       for (size_t i = 1; trace_ev && i < tev.size(); ++i) {
         float ms = 0.f;

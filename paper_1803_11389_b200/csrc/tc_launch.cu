@@ -365,10 +365,10 @@ cudaError_t tc_layer_run(int cell, int mode, TcArgs a, const void* Wtc, int Kp, 
   if (a.split_start <= 0 || a.split_start > nitems || mode != TC_3XTF32) a.split_start = nitems;
   if (grid_out) *grid_out = grid;
   if (cell == LINEAR) {
-    // dense layers: bf16 / tf32 products (fp32 layers run the FFMA kernel)
+    // dense layers: bf16 / tf32 products, or 3xTF32 for fp32 layers large enough to fill the GPU
     if (mode == TC_BF16) return run_n<LINEAR, TC_BF16>(N, a, tw, tx, grid, s);
     if (mode == TC_TF32) return run_n<LINEAR, TC_TF32>(N, a, tw, tx, grid, s);
-    return cudaErrorInvalidValue;
+    return run_n<LINEAR, TC_3XTF32>(N, a, tw, tx, grid, s);  // fp32 dense layers: fp32-accurate split products
   }
   if (cell == SRU) {
     if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tw, tx, grid, s);
@@ -387,7 +387,7 @@ cudaError_t tc_layer_preload(int cell, int mode, int T_b) {
   if (cell == LINEAR) {
     if (mode == TC_BF16) return run_n<LINEAR, TC_BF16>(N, a, tm, tm, 0, nullptr);
     if (mode == TC_TF32) return run_n<LINEAR, TC_TF32>(N, a, tm, tm, 0, nullptr);
-    return cudaErrorInvalidValue;
+    return run_n<LINEAR, TC_3XTF32>(N, a, tm, tm, 0, nullptr);
   }
   if (cell == SRU) {
     if (mode == TC_BF16) return run_n<SRU, TC_BF16>(N, a, tm, tm, 0, nullptr);

@@ -761,7 +761,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         continue;
       }
-      if constexpr (CELL == LINEAR) {
+      if constexpr (CELL == LINEAR && !C::CHUNKED) {
         // dense layer: gate plane g holds output columns [g*Hpad, (g+1)*Hpad);
         // accumulators + bias straight to Y (a warp stores 128 contiguous bytes per row)
         const int ab = acc_it % C::NACC;
@@ -872,9 +872,26 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
         }
+        if constexpr (CELL == LINEAR) {
+          // dense layer on the fp32-accurate path: plane g holds output columns
+          // [g*Hpad, (g+1)*Hpad); chunk sums + bias straight to Y
+          float* const rg[3] = {rz, rf, ro};
+#pragma unroll
+          for (int g = 0; g < 3; ++g) {
+            const int col = g * a.Hpad + unit;
+            const bool lv = col < a.H;
+            const float bias = (lv && a.bias) ? a.bias[col] : 0.f;
+            float* yp = a.Hout + t0 * a.ldh + col;
+#pragma unroll
+            for (int j = 0; j < N; ++j)
+              if (lv && j < l) yp[(int64_t)j * a.ldh] = rg[g][j] + bias;
+          }
+          continue;
+        }
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-          if (CELL == SRU) {
+          if (a.dbg & 1024) {  // timing experiment: no activation math
+          } else if (CELL == SRU) {
             rf[j] = tc_sigmoid(rf[j] + bf);
             ro[j] = tc_sigmoid(ro[j] + br);
           } else {
@@ -890,9 +907,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           Bblk = rf[j] * Bblk + (1.f - rf[j]) * rz[j];
           Ablk = rf[j] * Ablk;
         }
-        const float cin = tc_lookback(a, b, u, unit, et, Ablk, Bblk);
+        const float cin = (a.dbg & 16) ? 0.f : tc_lookback(a, b, u, unit, et, Ablk, Bblk);  // 16: no look-back (timing)
         float c = cin;
-        const bool live = unit < a.H;
+        const bool live = unit < a.H && !(a.dbg & 512);  // 512: no stores (timing)
 #pragma unroll
         for (int j = 0; j < N; ++j) {  // the c chain alone (one FMA per step) ...
           c = rf[j] * c + (1.f - rf[j]) * rz[j];
