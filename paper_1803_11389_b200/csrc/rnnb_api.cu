@@ -387,7 +387,7 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   const char* env_sp = getenv("RNNB_TC_SPLIT");
   if (mode == TC_3XTF32 && !(env_sp && env_sp[0] == '0')) {
     int W = nitems / G, R = nitems - W * G;
-    const int nch = (a.nK + RNNB_X3_CK - 1) / RNNB_X3_CK;
+    const int nch = x3_nchunks(a.nK);
     if (streaming && nitems > G) {
       // input-bound launch (rows arrive slower than the kernel consumes them):
       // what counts is how soon the LAST blocks finish after their rows land,

@@ -430,6 +430,24 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
 #ifndef RNNB_X3_CK
 #define RNNB_X3_CK 8  // 3xTF32 K chunk in k-tiles (8 x 32 = 256-deep; 128-deep: 8 % slower, half the error)
 #endif
+#ifndef RNNB_X3_CK0
+#define RNNB_X3_CK0 RNNB_X3_CK  // the FIRST TWO chunks of an item may be longer (experiment, see below)
+#endif
+// 3xTF32 chunk plan of an item's nK k-tiles: two chunks of CK0 k-tiles, then
+// chunks of CK.  While the epilogue warps finish an item (activations,
+// look-back, scan, stores) the MMA warp can run only two chunks of the next
+// item ahead (two TMEM buffers; TMEM is full).  Longer first chunks (CK0 = 12)
+// were tried to buy slack there: cfg2 T_b=32 209.2 -> 205.8 us, but 25 % more
+// accumulation error (cfg2 9.8e-7 -> 1.2e-6, cfg4 4.2e-6 -> 4.6e-6) -- not
+// worth it, so CK0 = CK; the look-back's cost (~10 us per launch) is the tail
+// after the last wave, not a per-item stall.
+__host__ __device__ __forceinline__ int x3_chunk_start(int c) {
+  return c <= 2 ? c * RNNB_X3_CK0 : 2 * RNNB_X3_CK0 + (c - 2) * RNNB_X3_CK;
+}
+__host__ __device__ __forceinline__ int x3_chunk_of(int kt) {
+  return kt < 2 * RNNB_X3_CK0 ? kt / RNNB_X3_CK0 : 2 + (kt - 2 * RNNB_X3_CK0) / RNNB_X3_CK;
+}
+__host__ __device__ __forceinline__ int x3_nchunks(int nK) { return x3_chunk_of(nK - 1) + 1; }
 template <int MODE, int N>
 struct TcCfg {
   static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
@@ -503,7 +521,7 @@ __device__ __forceinline__ bool tc_work(const TcArgs& a, int nitems, int k, TcWo
     return true;
   }
   if (k == nwhole && a.split_start < nitems && bx < 2 * (nitems - a.split_start)) {
-    const int kmid = ((a.nK + CK - 1) / CK / 2) * CK;
+    const int kmid = x3_chunk_start(x3_nchunks(a.nK) / 2);
     const int part = bx & 1;
     w = TcWork{a.split_start + bx / 2, part ? kmid : 0, part ? a.nK : kmid, part};
     return true;
@@ -669,7 +687,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           tc_fence_after();
         }
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int kc = C::CHUNKED ? kt % C::CK : kt;  // k-tile index inside the accumulation
+          const int kch = C::CHUNKED ? x3_chunk_of(kt) : 0;
+          const int kc = C::CHUNKED ? kt - x3_chunk_start(kch) : kt;  // k-tile index inside the accumulation
+          const bool kc_last = C::CHUNKED && (kt + 1 == x3_chunk_start(kch + 1) || kt == w.kt1 - 1);
           if (C::CHUNKED && kc == 0) {  // a new K-chunk accumulates into a fresh buffer
             ab = acc_it % C::NACC;
             dbase = tmem + ab * C::ACC_COLS;
@@ -704,7 +724,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               tc_commit_elect(&empty[wb + 2]);
               tc_commit_elect(&empty[C::NW + xs]);
             }
-            if (kc == C::CK - 1 || kt == w.kt1 - 1) {
+            if (kc_last) {
               tc_commit_elect(&acc_full[ab]);  // this K-chunk's partial products complete
               ++acc_it;
             }
@@ -719,7 +739,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                                  C::CHUNKED ? idesc_2n : idesc, kc != 0, N, idesc_n,
                                  (uint64_t)((3 * C::A_BYTES) >> 4));
           tc_commit_elect(&empty[s]);  // frees the smem stage once these MMAs have read it
-          if (C::CHUNKED && (kc == C::CK - 1 || kt == w.kt1 - 1)) {
+          if (kc_last) {
             tc_commit_elect(&acc_full[ab]);  // this K-chunk's partial products complete
             ++acc_it;
           }
@@ -751,7 +771,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       const int unit = u * 128 + row;
       if (a.dbg & 32) {  // timing experiment: epilogue only hands the accumulators back
-        const int nacc = C::CHUNKED ? (w.kt1 - w.kt0 + C::CK - 1) / C::CK : 1;
+        const int nacc = C::CHUNKED ? x3_chunk_of(w.kt1 - 1) - x3_chunk_of(w.kt0) + 1 : 1;
         for (int ch = 0; ch < nacc; ++ch, ++acc_it) {
           const int ab = acc_it % C::NACC;
           mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
@@ -798,7 +818,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         float rz[N], rf[N], ro[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) rz[j] = rf[j] = ro[j] = 0.f;
-        const int nch = (a.nK + C::CK - 1) / C::CK;
+        const int nch = x3_nchunks(a.nK);
         const int hch = nch / 2;  // first chunk of the second half (see tc_work)
         const int c_lo = w.part == 1 ? hch : 0, c_hi = w.part == 0 ? hch : nch;
         // the first half's sum waits in TMEM columns past the accumulators
