@@ -13,6 +13,23 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1803_11389_b200 as P  # noqa: E402
 from paper_1803_11389_b200 import workloads  # noqa: E402
 
+def bind_to_gpu_numa_node(index=0):
+    """Pin this process to the CPU cores NVML reports as local to the GPU, so
+    pinned host buffers are first-touched on the GPU's NUMA node."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        n = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (n + 63) // 64)
+        cpus = [64 * i + b for i, wd in enumerate(words) for b in range(64) if (wd >> b) & 1 and 64 * i + b < n]
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+        return cpus
+    except Exception as e:  # noqa: BLE001
+        return f"unavailable: {e}"
+
+
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="cfg2")
 ap.add_argument("--block", type=int, default=32)
@@ -20,6 +37,9 @@ ap.add_argument("--mode", default="f32")
 ap.add_argument("--reps", type=int, default=50)
 ap.add_argument("--tag", default="")
 a = ap.parse_args()
+if os.environ.get("E2E_BIND"):
+    print("bound to cpus", bind_to_gpu_numa_node(), flush=True)
+print("affinity", sorted(os.sched_getaffinity(0))[:4], "...", len(os.sched_getaffinity(0)), "cpus", flush=True)
 w = workloads.make(a.workload)
 st = P.DeviceStack(w.kind, w.layers, mode=a.mode)
 Xh = torch.from_numpy(w.X.astype(st.np_dtype)).pin_memory()
