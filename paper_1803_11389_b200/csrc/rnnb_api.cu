@@ -350,8 +350,15 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   (void)nst;
   int* status = h->tc_status;
   ++h->tc_epoch;
+  // the look-back arrays start as all-ones sentinels: filled by the operand
+  // conversion kernel (no extra launch), or by a memset when the conversion
+  // streams beside the layer kernel
+  const size_t lb_bytes = 3 * plane * sizeof(float);
   if (!streaming)
-    CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s));
+    CUDA_TRY(tc_to_operand(mode, X, ldx, h->kind == RNNB_QRNN ? xc_io : nullptr, h->op, ldop, L, (int)ly.din, s,
+                           aggA, lb_bytes));
+  else
+    CUDA_TRY(cudaMemsetAsync(aggA, 0xFF, lb_bytes, s));
   TcArgs a{};
   a.Xhw = X + ly.hw_off;
   a.ldhw = ldx;
@@ -364,9 +371,8 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.c_in = c_io;                          // read only (anchor of the look-back)
   a.c_out = c_io ? h->cbuf : nullptr;     // c_T to scratch, copied to c_io after the launch
   a.epoch = h->tc_epoch;
-  a.aggA = aggA;
-  a.aggB = aggA + plane;
-  a.incl = aggA + 2 * plane;
+  a.agg = reinterpret_cast<unsigned long long*>(aggA);
+  a.incl = reinterpret_cast<unsigned int*>(aggA + 2 * plane);
   a.status = status;
   a.L = L;
   a.T_b = (int)Tb;

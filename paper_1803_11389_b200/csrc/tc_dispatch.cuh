@@ -6,11 +6,14 @@
 namespace rnnb {
 
 // MMA-operand copy of a layer input with a leading x_{-1} row.
+// `fill` (16-byte multiple): the following layer launch's look-back state, set
+// to the all-ones sentinel by the same kernel (no extra launch)
 cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
-                          int64_t L, int D, cudaStream_t s);
+                          int64_t L, int D, cudaStream_t s, void* fill = nullptr, size_t fill_bytes = 0);
 // rows of a longer operand (3xTF32 lo plane prow rows after the hi plane)
 cudaError_t tc_to_operand_rows(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
-                               int64_t L, int D, int64_t prow, cudaStream_t s);
+                               int64_t L, int D, int64_t prow, cudaStream_t s, void* fill = nullptr,
+                               size_t fill_bytes = 0);
 
 // copy segments of a streamed input: segment j = X rows [end[j-1], end[j])
 constexpr int kMaxSegs = 48;

@@ -9,7 +9,11 @@ namespace rnnb {
 // the MMA operand type (bf16 RNE, or tf32 RNA kept in fp32 containers).
 template <int MODE>
 __global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ xcarry,
-                                  void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow) {
+                                  void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow,
+                                  uint4* __restrict__ fill, size_t fill16) {
+  // look-back state of the layer launch that follows: all-ones sentinel (tc_lookback)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < fill16; i += (size_t)gridDim.x * blockDim.x)
+    fill[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
   const int64_t n = (L + 1) * (int64_t)D;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / D;
@@ -32,7 +36,13 @@ __global__ void to_operand_kernel(const float* __restrict__ X, int64_t ldx, cons
 // ran at ~1.2 TB/s on cfg2).  Needs 16-byte aligned rows (host-checked).
 template <int MODE>
 __global__ void to_operand_v4_kernel(const float* __restrict__ X, int64_t ldx, const float* __restrict__ xcarry,
-                                     void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow) {
+                                     void* __restrict__ out, int64_t ldo, int64_t L, int D, int64_t prow,
+                                     uint4* __restrict__ fill, size_t fill16) {
+  {  // look-back state of the layer launch that follows: all-ones sentinel (tc_lookback)
+    const size_t nthr = (size_t)gridDim.x * gridDim.y * blockDim.x;
+    for (size_t i = ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x; i < fill16; i += nthr)
+      fill[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+  }
   const int nv = D >> 2;
   for (int64_t r = blockIdx.y; r <= L; r += gridDim.y) {
     const float* src = r == 0 ? xcarry : X + (r - 1) * ldx;
@@ -63,7 +73,9 @@ __global__ void to_operand_v4_kernel(const float* __restrict__ X, int64_t ldx, c
 // 3xTF32 lo plane starts prow rows after the hi plane (prow = L+1 for a whole
 // sequence; a row range of a longer operand passes that operand's L+1).
 cudaError_t tc_to_operand_rows(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
-                               int64_t L, int D, int64_t prow, cudaStream_t s) {
+                               int64_t L, int D, int64_t prow, cudaStream_t s, void* fill, size_t fill_bytes) {
+  uint4* f4 = static_cast<uint4*>(fill);
+  const size_t f16 = fill ? fill_bytes / 16 : 0;
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (D % 4 == 0 && ldx % 4 == 0 && ldo % 8 == 0 && al16(X) && (xcarry == nullptr || al16(xcarry)) && al16(out)) {
     const int nv = D / 4;
@@ -71,23 +83,23 @@ cudaError_t tc_to_operand_rows(int mode, const float* X, int64_t ldx, const floa
     const int64_t rows = L + 1;
     const int by = (int)(rows < 148 * 16 / bx ? rows : (148 * 16 / bx > 0 ? 148 * 16 / bx : 1));
     const dim3 grid(bx, by);
-    if (mode == TC_BF16) to_operand_v4_kernel<TC_BF16><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
-    else if (mode == TC_TF32) to_operand_v4_kernel<TC_TF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
-    else to_operand_v4_kernel<TC_3XTF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
+    if (mode == TC_BF16) to_operand_v4_kernel<TC_BF16><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow, f4, f16);
+    else if (mode == TC_TF32) to_operand_v4_kernel<TC_TF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow, f4, f16);
+    else to_operand_v4_kernel<TC_3XTF32><<<grid, 256, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow, f4, f16);
     return cudaGetLastError();
   }
   const int64_t n = (L + 1) * (int64_t)D;
   const int bs = 256;
   const int grid = (int)((n + bs - 1) / bs < 148 * 16 ? (n + bs - 1) / bs : 148 * 16);
-  if (mode == TC_BF16) to_operand_kernel<TC_BF16><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
-  else if (mode == TC_TF32) to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
-  else to_operand_kernel<TC_3XTF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow);
+  if (mode == TC_BF16) to_operand_kernel<TC_BF16><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow, f4, f16);
+  else if (mode == TC_TF32) to_operand_kernel<TC_TF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow, f4, f16);
+  else to_operand_kernel<TC_3XTF32><<<grid, bs, 0, s>>>(X, ldx, xcarry, out, ldo, L, D, prow, f4, f16);
   return cudaGetLastError();
 }
 
 cudaError_t tc_to_operand(int mode, const float* X, int64_t ldx, const float* xcarry, void* out, int64_t ldo,
-                          int64_t L, int D, cudaStream_t s) {
-  return tc_to_operand_rows(mode, X, ldx, xcarry, out, ldo, L, D, L + 1, s);
+                          int64_t L, int D, cudaStream_t s, void* fill, size_t fill_bytes) {
+  return tc_to_operand_rows(mode, X, ldx, xcarry, out, ldo, L, D, L + 1, s, fill, fill_bytes);
 }
 
 // Streaming conversion (rnnb_forward_host): ONE persistent launch converts

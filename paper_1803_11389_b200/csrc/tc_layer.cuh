@@ -50,12 +50,14 @@ struct TcArgs {
   const float* bias;  // SRU [Hpad][2] (b_forget, b_highway) or nullptr
   const float* c_in;  // [H] c_0 (nullptr: zeros); never written by the launch
   float* c_out;       // [H] c_T (nullptr: not written); must not alias c_in
-  int* status;        // [nB][nU] look-back status: 4*epoch + {1 aggregate, 2 inclusive}
+  int* status;        // split last wave's flags (fixflag) live at its end; tagged 4*epoch + 3
   int epoch;          // this launch's tag: values of earlier launches read as "none"
-                      // (no per-launch clearing of the status array)
-  float* aggA;        // [nB][Hpad] block carry map c_out = A c_in + B
-  float* aggB;
-  float* incl;        // [nB][Hpad] c after the block (inclusive prefix)
+  // look-back state, "the value is the flag": the launch's predecessor (the
+  // operand conversion, or a memset) fills both arrays with kLbSentinel bits
+  // (a NaN pattern the publishers never store), a published value is whatever
+  // differs from it
+  unsigned long long* agg;  // [nB][Hpad] block carry map c_out = A c_in + B as the pair (A, B)
+  unsigned int* incl;       // [nB][Hpad] c after the block (inclusive prefix), fp32 bits
   int64_t L;
   int T_b;
   int H, Hpad, D;
@@ -365,65 +367,77 @@ __device__ __forceinline__ void tc_count_done(const TcArgs& a, int64_t t0, int e
   }
 }
 
-// Publish block b's AGGREGATE carry map, run the deterministic fixed-depth
-// look-back (composes the aggregates of blocks b-1 .. b-kLB, in fixed order,
-// onto the INCLUSIVE carry of block b-kLB-1 or c_0 -- timing never changes
-// the arithmetic, so results are run-to-run and chunking/GPU-count
-// invariant), publish block b's INCLUSIVE carry and return c_in.  Called by
-// the 128 epilogue threads (et = 0..127, thread = unit of tile u).
+// Decoupled look-back, "the value is the flag".  Publish block b's AGGREGATE
+// carry map (A, B) as ONE 8-byte store, fetch the aggregates of blocks b-1 ..
+// b-kLB of the same unit (and the INCLUSIVE carry of block b-kLB-1, or c_0) --
+// each a single-copy-atomic load that is re-issued while it still returns the
+// sentinel the arrays were filled with before the launch -- compose them in
+// FIXED order (timing never changes the arithmetic: results are run-to-run
+// and chunking / GPU-count invariant), publish block b's inclusive carry and
+// return c_in.  Every thread works on its own unit: no barrier, no fence, no
+// status word; a ready predecessor costs one L2 round trip.  (The first
+// version published per-tile status words: store, barrier, release, 32 lanes
+// polling with acquires, barrier, loads -- three L2 round trips and two
+// barriers on every item's critical path: 14-26 % of a cfg2 bf16 launch at
+// T_b = 64-16.)  Real NaNs are re-coded so they can never equal the sentinel.
+constexpr unsigned int kLbSentinel = 0xFFFFFFFFu;
+__device__ __forceinline__ unsigned int lb_bits(float v) {
+  const unsigned int u = __float_as_uint(v);
+  return u == kLbSentinel ? 0x7FC00000u : u;
+}
+__device__ __forceinline__ unsigned long long lb_load64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int lb_load32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int unit, int et, float Ablk,
                                              float Bblk) {
+  (void)u;
+  (void)et;
   const size_t sidx = (size_t)b * a.Hpad + unit;
-  a.aggA[sidx] = Ablk;
-  a.aggB[sidx] = Bblk;
-  // the barrier orders the 128 threads' stores before thread 0's gpu-scope
-  // release (st.release = fence.acq_rel.gpu + store; cumulative over the
-  // writes the barrier ordered before it), one fence per item instead of 128
-  tc_epi_sync();
-  const int tag = 4 * a.epoch;
-  if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 1);
+  const unsigned long long mine = (unsigned long long)lb_bits(Ablk) | ((unsigned long long)lb_bits(Bblk) << 32);
+  asm volatile("st.relaxed.gpu.global.b64 [%0], %1;\n" ::"l"(a.agg + sidx), "l"(mine) : "memory");
   const int jlo = b - kLB > 0 ? b - kLB : 0;  // oldest aggregate used
-  // lanes of the first epilogue warp wait for the statuses in parallel
-  if (et < 32) {
-    const int j = b - 1 - et;
-    if (j >= jlo) while (ld_acquire(&a.status[(size_t)j * a.nU + u]) < tag + 1) __nanosleep(32);
-    const int jb = jlo - 1;  // block whose inclusive carry anchors the chain
-    if (et == 0 && jb >= 0) while (ld_acquire(&a.status[(size_t)jb * a.nU + u]) < tag + 2) __nanosleep(32);
-  }
-  tc_epi_sync();
-  // All kLB aggregates (and the anchor) are loaded at once -- constant
-  // register indices, identity maps (A = 1, B = 0) past jlo -- and composed
-  // afterwards in the fixed order j = b-1 .. jlo (one L2 round trip instead
-  // of kLB dependent ones).  The identity steps leave the composed map
-  // bitwise unchanged (x*1 and fma(x, 0, y) are exact).  The barrier above
-  // orders these plain L2 loads after warp 0's acquires (and the compiler
-  // cannot hoist them across it).
-  float Aj[kLB], Bj[kLB];
+  // all kLB loads (and the anchor) in flight at once, constant register
+  // indices; identity maps (A = 1, B = 0) past jlo leave the composed map
+  // bitwise unchanged (x*1 and fma(x, 0, y) are exact)
+  constexpr unsigned long long kPair = ((unsigned long long)kLbSentinel << 32) | kLbSentinel;
+  unsigned long long pj[kLB];
 #pragma unroll
   for (int k = 0; k < kLB; ++k) {
     const int j = b - 1 - k;
-    const bool v = j >= jlo;
-    const size_t jidx = (size_t)(v ? j : 0) * a.Hpad + unit;
-    Aj[k] = v ? __ldcg(&a.aggA[jidx]) : 1.f;
-    Bj[k] = v ? __ldcg(&a.aggB[jidx]) : 0.f;
+    pj[k] = j >= jlo ? lb_load64(a.agg + (size_t)j * a.Hpad + unit) : 0ull;
   }
-  const float anchor = jlo > 0 ? __ldcg(&a.incl[(size_t)(jlo - 1) * a.Hpad + unit])
-                                : (a.c_in != nullptr && unit < a.H ? a.c_in[unit] : 0.f);
+  unsigned int anc = 0;
+  if (jlo > 0) anc = lb_load32(a.incl + (size_t)(jlo - 1) * a.Hpad + unit);
+#pragma unroll
+  for (int k = 0; k < kLB; ++k) {
+    const int j = b - 1 - k;
+    if (j >= jlo)
+      while (pj[k] == kPair) pj[k] = lb_load64(a.agg + (size_t)j * a.Hpad + unit);
+  }
+  if (jlo > 0)
+    while (anc == kLbSentinel) anc = lb_load32(a.incl + (size_t)(jlo - 1) * a.Hpad + unit);
+  const float anchor = jlo > 0 ? __uint_as_float(anc) : (a.c_in != nullptr && unit < a.H ? a.c_in[unit] : 0.f);
   float Aacc = 1.f, Bacc = 0.f;  // map from c after block jlo-1 to c after block b-1
 #pragma unroll
   for (int k = 0; k < kLB; ++k) {
-    Bacc = Aacc * Bj[k] + Bacc;
-    Aacc = Aacc * Aj[k];
+    const bool v = b - 1 - k >= jlo;
+    const float Aj = v ? __uint_as_float((unsigned int)pj[k]) : 1.f;
+    const float Bj = v ? __uint_as_float((unsigned int)(pj[k] >> 32)) : 0.f;
+    Bacc = Aacc * Bj + Bacc;
+    Aacc = Aacc * Aj;
   }
   const float cin = Aacc * anchor + Bacc;
-  // the INCLUSIVE carry is only ever read as the anchor of block b+kLB+1:
-  // the last kLB+1 blocks skip its store, barrier and release (one gpu-scope
-  // fence and an L2 round trip per item; every block of a cfg2 T_b=64 launch)
-  if (b + kLB + 1 < a.nB) {
-    a.incl[sidx] = Ablk * cin + Bblk;
-    tc_epi_sync();
-    if (et == 0) st_release(&a.status[(size_t)b * a.nU + u], tag + 2);
-  }
+  // the INCLUSIVE carry is only ever read as the anchor of block b+kLB+1
+  if (b + kLB + 1 < a.nB)
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;\n" ::"l"(a.incl + sidx), "r"(lb_bits(Ablk * cin + Bblk))
+                 : "memory");
   return cin;
 }
 
