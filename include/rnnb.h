@@ -112,12 +112,14 @@ rnnb_status rnnb_forward(rnnb_stack_t h, const void* X, int64_t ldx, int64_t L, 
                          void* H, int64_t ldh, void* c_state, void* x_carry, void* stream);
 
 /* Same on HOST buffers: H2D of X, forward, D2H of H inside the call
- * (pinned or pageable).  Copies overlap compute: single-layer fp32 stacks
- * stream (one layer launch consumes X rows as a copy stream lands them and
- * publishes finished h chunks to a copy-out stream); other stacks run a
- * chunked copy-in / forward / copy-out pipeline at block boundaries.
- * Results are bitwise those of rnnb_forward.  Synchronises the stream
- * before returning. */
+ * (pinned or pageable).  Copies overlap compute: single-layer stacks stream
+ * (one layer launch consumes X rows as copy streams land them; when H is
+ * pinned, i.e. device-mapped, host memory the kernel stores h straight into
+ * it, otherwise finished h granules go out on a copy-out stream); other
+ * stacks run a chunked copy-in / forward / copy-out pipeline at block
+ * boundaries.  Results are bitwise those of rnnb_forward.  Synchronises the
+ * stream before returning.  A stack handle must not be used by two calls
+ * at once. */
 rnnb_status rnnb_forward_host(rnnb_stack_t h, const void* X, int64_t L, int64_t block_size,
                               void* H, void* c_state, void* x_carry, void* stream);
 
