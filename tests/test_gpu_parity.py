@@ -616,6 +616,34 @@ def test_host_streaming_pinned_buffers_zero_copy_output(P, oracle, kind, mode, d
     st.close()
 
 
+@pytest.mark.timeout(120)
+@pytest.mark.parametrize("mode,T", [("bf16", 16), ("f32", 32), ("tf32", 64)])
+def test_lookback_sentinel_never_collides_with_data(P, oracle, mode, T):
+    """The look-back publishes carry maps by value into arrays pre-filled with
+    an all-ones sentinel and consumers wait until a value differs from it: NaN
+    inputs -- including the NaN whose bits ARE the sentinel -- must not hang
+    the launch (published NaNs are re-coded) and must leave every step before
+    the first NaN row bitwise equal to the clean run; the next launch on the
+    same stack is clean again."""
+    import torch
+    d, L = 512, 40 * T + 5
+    layers = oracle.generate_layers("qrnn", d, d, 1, 97, np.float32)
+    X = np.random.default_rng(31).standard_normal((L, d)).astype(np.float32)
+    st = P.DeviceStack("qrnn", layers, mode=mode)
+    clean = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
+    assert st.query(9) == 1
+    bad = X.copy()
+    t_bad = 17 * T + 3
+    bad[t_bad, :] = np.frombuffer(np.uint32(0xFFFFFFFF).tobytes(), np.float32)[0]
+    bad[t_bad + 1, ::2] = np.nan
+    H = st.forward(torch.from_numpy(bad).cuda(), T).cpu().numpy()  # must return
+    assert H[:t_bad].tobytes() == clean[:t_bad].tobytes()
+    assert H.shape == clean.shape  # (what a NaN step yields is not specified: the branch-free activations saturate it)
+    again = st.forward(torch.from_numpy(X).cuda(), T).cpu().numpy()
+    assert again.tobytes() == clean.tobytes()
+    st.close()
+
+
 @pytest.mark.parametrize("kind,d,L", [("qrnn", 1024, 2048), ("sru", 1024, 3000), ("qrnn", 2048, 700)])
 def test_split_last_wave_is_bitwise_neutral(P, oracle, kind, d, L, monkeypatch):
     """3xTF32: the last partial wave's items run as two K halves on two CTAs
