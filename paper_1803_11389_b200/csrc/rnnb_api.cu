@@ -184,6 +184,64 @@ uint16_t to_bf16(float v) {
   return (uint16_t)(u >> 16);
 }
 
+// Weight repack on the GPU: the caller's gate matrices are staged in device
+// memory as they are and ONE kernel writes both device layouts (gate-
+// interleaved FFMA rows, gate-major tensor-core planes) with the mode's
+// rounding -- the host used to do this element by element (40-50 ms for cfg2,
+// which made the reference-signature run_blocked, one upload per call, slower
+// than the CPU reference).
+struct PackArgs {
+  const void* m[6];   // SRU: W, W_f, W_r, b_f, b_r ; QRNN: (cand, forget, out) x (tap 0, tap 1)
+  int kind, mode, T;
+  int64_t dh, din, Dp, Kp;        // FFMA layout W[3*Upad][Kp], row 3u+g, columns [tap][Dp]
+  void* W;
+  void* Wtc;                      // tensor-core layout [planes][3*Hpad][tcKp], row g*Hpad+u, columns [tap][Dtc]
+  int64_t Hpad, tcKp, Dtc, lo_off;  // lo_off: elements from the hi to the lo plane (3xTF32), 0: one plane
+  void* bias;                     // SRU [Upad][2] in the stack's element type
+  float* bias_tc;                 // SRU [Hpad][2]
+};
+template <typename S>
+__global__ void pack_layer_kernel(const PackArgs a) {
+  const int64_t n = a.dh * 3 * a.T * a.din;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = i % a.din;
+    int64_t r = i / a.din;
+    const int tap = (int)(r % a.T);
+    r /= a.T;
+    const int g = (int)(r % 3);
+    const int64_t u = r / 3;
+    const int slot = a.kind == RNNB_SRU ? g : 2 * g + tap;
+    const double v = (double)static_cast<const S*>(a.m[slot])[u * a.din + k];
+    const float vf = (float)v;
+    const int64_t dst = (3 * u + g) * a.Kp + (int64_t)tap * a.Dp + k;
+    switch (a.mode) {
+      case RNNB_F64: static_cast<double*>(a.W)[dst] = v; break;
+      case RNNB_BF16: static_cast<__nv_bfloat16*>(a.W)[dst] = __float2bfloat16_rn(vf); break;
+      case RNNB_TF32: static_cast<float*>(a.W)[dst] = rnnb::round_x(vf, rnnb::XR_TF32); break;
+      default: static_cast<float*>(a.W)[dst] = vf; break;
+    }
+    if (a.Wtc) {
+      const int64_t d2 = ((int64_t)g * a.Hpad + u) * a.tcKp + (int64_t)tap * a.Dtc + k;
+      if (a.mode == RNNB_BF16) {
+        static_cast<__nv_bfloat16*>(a.Wtc)[d2] = __float2bfloat16_rn(vf);
+      } else {
+        const float hi = rnnb::round_x(vf, rnnb::XR_TF32);
+        static_cast<float*>(a.Wtc)[d2] = hi;
+        if (a.lo_off) static_cast<float*>(a.Wtc)[d2 + a.lo_off] = rnnb::round_x(vf - hi, rnnb::XR_TF32);
+      }
+    }
+  }
+  if (a.kind == RNNB_SRU)
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.dh * 2; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t u = i >> 1;
+      const int j = (int)(i & 1);
+      const double v = (double)static_cast<const S*>(a.m[3 + j])[u];
+      if (a.mode == RNNB_F64) static_cast<double*>(a.bias)[i] = v;
+      else static_cast<float*>(a.bias)[i] = (float)v;
+      if (a.bias_tc) a.bias_tc[i] = (float)v;
+    }
+}
+
 rnnb_status ensure_ws(rnnb_stack* h, size_t bytes) {
   if (h->ws_bytes >= bytes) return RNNB_OK;
   for (auto& p : h->ws)
@@ -695,50 +753,47 @@ static rnnb_status rnnb_stack_set_layer_impl(rnnb_stack_t h, int layer, const vo
   const int T = taps(h->kind);
   const int64_t Kp = (int64_t)T * ly.Dp;
   const int64_t rows = (int64_t)ly.Upad * 3;
-  auto get = [&](int m, int64_t idx) -> double {
-    return src_dtype == RNNB_DT_F64 ? static_cast<const double*>(mats[m])[idx]
-                                    : (double)static_cast<const float*>(mats[m])[idx];
-  };
-  // canonical index of (gate g, tap) -> mats slot
-  auto slot = [&](int g, int tap) { return h->kind == RNNB_SRU ? g : 2 * g + tap; };
   const size_t ws = wsize(h->mode);
-  std::vector<unsigned char> host((size_t)rows * Kp * ws, 0);
-  for (int64_t u = 0; u < ly.dh; ++u)
-    for (int g = 0; g < 3; ++g)
-      for (int tap = 0; tap < T; ++tap) {
-        const int m = slot(g, tap);
-        const int64_t r = 3 * u + g;
-        for (int64_t k = 0; k < ly.din; ++k) {
-          const double v = get(m, u * ly.din + k);
-          const size_t dst = (size_t)r * Kp + (size_t)tap * ly.Dp + k;
-          switch (h->mode) {
-            case RNNB_F64: reinterpret_cast<double*>(host.data())[dst] = v; break;
-            case RNNB_BF16: reinterpret_cast<uint16_t*>(host.data())[dst] = to_bf16((float)v); break;
-            case RNNB_TF32: reinterpret_cast<float*>(host.data())[dst] = to_tf32((float)v); break;
-            default: reinterpret_cast<float*>(host.data())[dst] = (float)v; break;
-          }
-        }
-      }
+  const size_t ses = src_dtype == RNNB_DT_F64 ? 8 : 4;
   DeviceGuard dg(h->device);
   CUDA_TRY(dg.err);
-  if (ly.W) cudaFree(ly.W), ly.W = nullptr;
-  if (ly.Wst) cudaFree(ly.Wst), ly.Wst = nullptr;  // rebuilt from the new weights on first use
-  if (ly.bias) cudaFree(ly.bias), ly.bias = nullptr;
-  ly.wbytes = host.size();
-  CUDA_TRY(cudaMalloc(&ly.W, host.size()));
-  CUDA_TRY(cudaMemcpy(ly.W, host.data(), host.size(), cudaMemcpyHostToDevice));
+  for (void** p : {(void**)&ly.W, (void**)&ly.Wst, (void**)&ly.bias, (void**)&ly.Wtc, (void**)&ly.bias_tc})
+    if (*p) cudaFree(*p), *p = nullptr;  // (Wst: rebuilt from the new weights on first use)
+  // stage the caller's arrays as they are (one allocation)
+  const size_t mat_b = (size_t)ly.dh * ly.din * ses, vec_b = (size_t)ly.dh * ses;
+  size_t off[6], total = 0;
+  for (int i = 0; i < n_mats; ++i) {
+    off[i] = total;
+    total += ((h->kind == RNNB_SRU && i >= 3 ? vec_b : mat_b) + 255) / 256 * 256;
+  }
+  char* stage = nullptr;
+  CUDA_TRY(cudaMalloc(&stage, total));
+  struct StageFree {
+    char* p;
+    ~StageFree() { cudaFree(p); }
+  } stage_free{stage};
+  for (int i = 0; i < n_mats; ++i)
+    CUDA_TRY(cudaMemcpy(stage + off[i], mats[i], h->kind == RNNB_SRU && i >= 3 ? vec_b : mat_b, cudaMemcpyHostToDevice));
+  PackArgs pa{};
+  for (int i = 0; i < n_mats; ++i) pa.m[i] = stage + off[i];
+  pa.kind = h->kind;
+  pa.mode = h->mode;
+  pa.T = T;
+  pa.dh = ly.dh;
+  pa.din = ly.din;
+  pa.Dp = ly.Dp;
+  pa.Kp = Kp;
+  const size_t wb = (size_t)rows * Kp * ws;
+  CUDA_TRY(cudaMalloc(&ly.W, wb));
+  CUDA_TRY(cudaMemsetAsync(ly.W, 0, wb, 0));  // padding rows / columns
+  pa.W = ly.W;
+  ly.wbytes = wb;
   if (h->kind == RNNB_SRU) {
-    const size_t es = elem_size(h->mode);
-    std::vector<unsigned char> b((size_t)ly.Upad * 2 * es, 0);
-    for (int64_t u = 0; u < ly.dh; ++u)
-      for (int j = 0; j < 2; ++j) {
-        const double v = get(3 + j, u);
-        if (es == 8) reinterpret_cast<double*>(b.data())[u * 2 + j] = v;
-        else reinterpret_cast<float*>(b.data())[u * 2 + j] = (float)v;
-      }
-    CUDA_TRY(cudaMalloc(&ly.bias, b.size()));
-    CUDA_TRY(cudaMemcpy(ly.bias, b.data(), b.size(), cudaMemcpyHostToDevice));
-    ly.wbytes += b.size();
+    const size_t bb = (size_t)ly.Upad * 2 * elem_size(h->mode);
+    CUDA_TRY(cudaMalloc(&ly.bias, bb));
+    CUDA_TRY(cudaMemsetAsync(ly.bias, 0, bb, 0));
+    pa.bias = ly.bias;
+    ly.wbytes += bb;
   }
   if (h->mode == RNNB_BF16 || h->mode == RNNB_TF32 || h->mode == RNNB_F32X3 || h->mode == RNNB_F32) {
     // tensor-core layout: rows (p*3 + g)*Hpad128 + u (plane p: hi / lo for
@@ -749,38 +804,27 @@ static rnnb_status rnnb_stack_set_layer_impl(rnnb_stack_t h, int layer, const vo
     ly.Hpad128 = (int)((ly.dh + 127) / 128 * 128);
     ly.tcKp = (int)(T * Dtc);
     const size_t rows_tc = (size_t)3 * ly.Hpad128;
-    std::vector<unsigned char> tc(planes * rows_tc * ly.tcKp * ws, 0);
-    for (int g = 0; g < 3; ++g)
-      for (int64_t u = 0; u < ly.dh; ++u)
-        for (int tap = 0; tap < T; ++tap) {
-          const int m = slot(g, tap);
-          for (int64_t k = 0; k < ly.din; ++k) {
-            const float v = (float)get(m, u * ly.din + k);
-            const size_t dst = ((size_t)g * ly.Hpad128 + u) * ly.tcKp + (size_t)tap * Dtc + k;
-            if (h->mode == RNNB_BF16) {
-              reinterpret_cast<uint16_t*>(tc.data())[dst] = to_bf16(v);
-            } else if (h->mode == RNNB_TF32) {
-              reinterpret_cast<float*>(tc.data())[dst] = to_tf32(v);
-            } else {
-              const float hi = to_tf32(v);
-              reinterpret_cast<float*>(tc.data())[dst] = hi;
-              reinterpret_cast<float*>(tc.data())[dst + rows_tc * ly.tcKp] = to_tf32(v - hi);
-            }
-          }
-        }
-    if (ly.Wtc) cudaFree(ly.Wtc), ly.Wtc = nullptr;
-    if (ly.bias_tc) cudaFree(ly.bias_tc), ly.bias_tc = nullptr;
-    CUDA_TRY(cudaMalloc(&ly.Wtc, tc.size()));
-    CUDA_TRY(cudaMemcpy(ly.Wtc, tc.data(), tc.size(), cudaMemcpyHostToDevice));
-    ly.wbytes += tc.size();
+    const size_t tb = planes * rows_tc * ly.tcKp * ws;
+    CUDA_TRY(cudaMalloc(&ly.Wtc, tb));
+    CUDA_TRY(cudaMemsetAsync(ly.Wtc, 0, tb, 0));
+    pa.Wtc = ly.Wtc;
+    pa.Hpad = ly.Hpad128;
+    pa.tcKp = ly.tcKp;
+    pa.Dtc = Dtc;
+    pa.lo_off = planes == 2 ? (int64_t)(rows_tc * ly.tcKp) : 0;
+    ly.wbytes += tb;
     if (h->kind == RNNB_SRU) {
-      std::vector<float> b((size_t)ly.Hpad128 * 2, 0.f);
-      for (int64_t u = 0; u < ly.dh; ++u)
-        for (int j = 0; j < 2; ++j) b[u * 2 + j] = (float)get(3 + j, u);
-      CUDA_TRY(cudaMalloc(&ly.bias_tc, b.size() * sizeof(float)));
-      CUDA_TRY(cudaMemcpy(ly.bias_tc, b.data(), b.size() * sizeof(float), cudaMemcpyHostToDevice));
+      CUDA_TRY(cudaMalloc(&ly.bias_tc, (size_t)ly.Hpad128 * 2 * sizeof(float)));
+      CUDA_TRY(cudaMemsetAsync(ly.bias_tc, 0, (size_t)ly.Hpad128 * 2 * sizeof(float), 0));
+      pa.bias_tc = ly.bias_tc;
     }
   }
+  const int64_t n = ly.dh * 3 * T * ly.din;
+  const int grid = (int)((n + 255) / 256 < 148 * 16 ? (n + 255) / 256 : 148 * 16);
+  if (src_dtype == RNNB_DT_F64) pack_layer_kernel<double><<<grid, 256>>>(pa);
+  else pack_layer_kernel<float><<<grid, 256>>>(pa);
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaStreamSynchronize(0));
   ly.loaded = true;
   return RNNB_OK;
 }
