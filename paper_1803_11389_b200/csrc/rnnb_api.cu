@@ -81,9 +81,9 @@ struct rnnb_stack {
   size_t rev_bytes = 0;
   void* op = nullptr;     // tensor-core operand copy of a layer input, [L+1][maxD]
   size_t op_bytes = 0;
-  float* cbuf = nullptr;  // tensor-core c_T scratch + look-back state + status words
-  int tc_epoch = 0;       // launch tag of the look-back status words
-  int* tc_status = nullptr;  // [capacity] status words, cleared only on (re)allocation
+  float* cbuf = nullptr;  // tensor-core c_T scratch + look-back state (carry maps, inclusive carries)
+  int tc_epoch = 0;       // launch tag of the split-last-wave flags
+  int* tc_status = nullptr;  // [kFixSlots] split-last-wave flags, cleared only on (re)allocation
   size_t tc_status_n = 0;
   float* fix = nullptr;      // 3xTF32 split last wave: first halves' chunk sums
   size_t fix_bytes = 0;
@@ -163,25 +163,6 @@ int choose_units(int64_t dh, int num_sms) {
   if (dh >= 4LL * num_sms * 0.85) return 4;
   if (dh > 2LL * num_sms) return 4;
   return 2;
-}
-
-float to_tf32(float v) {
-  uint32_t u;
-  std::memcpy(&u, &v, 4);
-  if ((u & 0x7f800000u) != 0x7f800000u) {  // round-to-nearest, ties away (cvt.rna)
-    u += 0x1000u;
-    u &= 0xffffe000u;
-  }
-  float r;
-  std::memcpy(&r, &u, 4);
-  return r;
-}
-uint16_t to_bf16(float v) {
-  uint32_t u;
-  std::memcpy(&u, &v, 4);
-  if ((u & 0x7f800000u) == 0x7f800000u) return (uint16_t)((u >> 16) | ((u & 0xffff) ? 0x40 : 0));
-  u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
-  return (uint16_t)(u >> 16);
 }
 
 // Weight repack on the GPU: the caller's gate matrices are staged in device
@@ -341,7 +322,7 @@ rnnb_status ensure_tc_op(rnnb_stack* h, int li, int64_t L, int64_t* ldop_out) {
   return RNNB_OK;
 }
 
-// + kFixSlots words after the look-back statuses: the split last wave's flags
+// flags of the split last wave (one per split item)
 constexpr size_t kFixSlots = 128;
 
 // Scratch of one tensor-core layer launch, (re)allocated when too small.
@@ -358,18 +339,17 @@ rnnb_status tc_layer_scratch(rnnb_stack* h, Layer& ly, int64_t nB, int nU, int N
     CUDA_TRY(cudaMalloc(&h->cbuf, cfb));
     h->cf_bytes = cfb;
   }
-  // status words [nB][nU] in their own allocation, cleared only when it is
-  // (re)allocated: each launch tags its statuses 4*epoch + state, so anything
-  // an earlier launch left (any layer, any layout) reads as "not yet"
-  const size_t nst = (size_t)nB * nU;
-  // + kFixSlots words after the look-back statuses: the split last wave's flags
-  if (h->tc_status_n < nst + kFixSlots || h->tc_epoch >= (1 << 28)) {
-    if (h->tc_status_n < nst + kFixSlots) {
+  // the split last wave's kFixSlots flags, tagged 4*epoch + 3 by each launch
+  // (cleared only when allocated or when the epoch wraps); the look-back
+  // itself needs no status words any more (tc_lookback)
+  (void)nU;
+  if (h->tc_status_n < kFixSlots || h->tc_epoch >= (1 << 28)) {
+    if (h->tc_status_n < kFixSlots) {
       if (h->tc_status) cudaFree(h->tc_status);
       h->tc_status = nullptr;
       h->tc_status_n = 0;
-      CUDA_TRY(cudaMalloc(&h->tc_status, (nst + kFixSlots) * sizeof(int)));
-      h->tc_status_n = nst + kFixSlots;
+      CUDA_TRY(cudaMalloc(&h->tc_status, kFixSlots * sizeof(int)));
+      h->tc_status_n = kFixSlots;
     }
     CUDA_TRY(cudaMemsetAsync(h->tc_status, 0, h->tc_status_n * sizeof(int), s));
     h->tc_epoch = 0;
@@ -404,9 +384,6 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   if (sst != RNNB_OK) return sst;
   const size_t plane = (size_t)nB * ly.Hpad128;
   float* aggA = h->cbuf + ly.Hpad128;
-  const size_t nst = (size_t)nB * nU;
-  (void)nst;
-  int* status = h->tc_status;
   ++h->tc_epoch;
   // the look-back arrays start as all-ones sentinels: filled by the operand
   // conversion kernel (no extra launch), or by a memset when the conversion
@@ -431,7 +408,6 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.epoch = h->tc_epoch;
   a.agg = reinterpret_cast<unsigned long long*>(aggA);
   a.incl = reinterpret_cast<unsigned int*>(aggA + 2 * plane);
-  a.status = status;
   a.L = L;
   a.T_b = (int)Tb;
   a.H = (int)ly.dh;
@@ -462,7 +438,7 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
     if (W >= 1 && R > 0 && 2 * R <= G && R <= (int)kFixSlots && nch >= 2) {
       a.split_start = nitems - R;
       a.fix = h->fix;
-      a.fixflag = status + (h->tc_status_n - kFixSlots);
+      a.fixflag = h->tc_status;
     }
   }
   int grid = 0;

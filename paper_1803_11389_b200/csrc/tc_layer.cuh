@@ -18,10 +18,10 @@
 // time blocks' projections run concurrently on different SMs (the weights of
 // a layer stay L2-resident and are re-read once per block, the reference's
 // "one weight fetch per block" model); only the cheap scan is chained: the
-// epilogue of (u, b) waits for the c state published by (u, b-1) through a
-// per-tile flag (acquire/release at gpu scope).  Items are claimed in
-// increasing order and every dependency points to a smaller item, so with
-// all CTAs co-resident the chain cannot deadlock.
+// epilogue of (u, b) composes the carry maps earlier blocks of the same unit
+// published (decoupled look-back, tc_lookback: the value is the flag).  Items
+// are claimed in increasing order and every dependency points to a smaller
+// item, so with all CTAs co-resident the chain cannot deadlock.
 //
 // Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
 // issuer (the converged warp; elect.sync picks the issuing lane), warps 2..5
@@ -50,8 +50,8 @@ struct TcArgs {
   const float* bias;  // SRU [Hpad][2] (b_forget, b_highway) or nullptr
   const float* c_in;  // [H] c_0 (nullptr: zeros); never written by the launch
   float* c_out;       // [H] c_T (nullptr: not written); must not alias c_in
-  int* status;        // split last wave's flags (fixflag) live at its end; tagged 4*epoch + 3
-  int epoch;          // this launch's tag: values of earlier launches read as "none"
+  int epoch;          // this launch's tag of the split-last-wave flags (fixflag holds 4*epoch + 3):
+                      // values of earlier launches read as "none"
   // look-back state, "the value is the flag": the launch's predecessor (the
   // operand conversion, or a memset) fills both arrays with kLbSentinel bits
   // (a NaN pattern the publishers never store), a published value is whatever
