@@ -186,7 +186,9 @@ __device__ __forceinline__ void tc_issue_ktile(uint32_t d0, uint64_t a0, uint64_
 // W_lo . x_hi into [d+N, d+2N)).  One block per k-tile, not per gate: every
 // asm block costs ptxas ~60 uniform-datapath instructions of operand set-up
 // that the tensor pipe's short queue does not hide (per-gate blocks: MMA-only
-// time 151 -> 189 us on cfg2).
+// time 151 -> 189 us on cfg2).  Releasing in two halves of three tiles (one
+// mid-stream commit instead of three) was measured too: 201 vs 198 us -- the
+// finer release is worth more than the commits cost.
 #define RNNB_G3STEP(ACCP)                                                   \
   "@e tcgen05.mma.cta_group::1.kind::tf32 [d], a, b, %3, " ACCP ";\n\t"     \
   "add.s64 al, a, 1024;\n\t@e tcgen05.mma.cta_group::1.kind::tf32 [dc], al, b, %6, 1;\n\t"
