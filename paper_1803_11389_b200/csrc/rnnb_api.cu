@@ -419,6 +419,16 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   a.nU = nU;
   a.nB = (int)nB;
   a.dbg = getenv("RNNB_DEBUG") ? atoi(getenv("RNNB_DEBUG")) : 0;
+  {
+    // second epilogue warp group (bf16 / tf32): when an item's MMA stream is
+    // shorter than ~8 us (51.3 cycles per MMA, 12 per k-tile) or the blocks are
+    // tiny, the epilogue bounds the item (measured: cfg3 K = 1024 +15..56 %,
+    // cfg2 K = 2048 -6..+3 % except T_b <= 4)
+    const double mma_us = (double)a.nK * 12 * 51.3 / 1965.0;
+    const char* eg = getenv("RNNB_TC_EGROUPS");
+    // (SRU's epilogue also gathers the highway x: cfg3 tf32, 10 us of MMAs per item, still gains 37 %)
+    a.egroups = eg ? atoi(eg) : ((mma_us < 8.0 || Tb <= 4 || (h->kind == RNNB_SRU && mma_us < 14.0)) ? 2 : 1);
+  }
   // 3xTF32: split the last, partial wave's items in two K halves on two CTAs
   // (tc_work in tc_layer.cuh; the arithmetic is the same split or not)
   const int nitems = nU * (int)nB;

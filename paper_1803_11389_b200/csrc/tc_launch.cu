@@ -305,11 +305,21 @@ static bool make_map(CUtensorMap* tm, CUtensorMapDataType dt, int es, const void
 // grid == 0: only load the kernel and set its attribute (CUDA loads kernel code
 // lazily at the first launch, and that load waits for the device -- fatal for
 // a first launch made while another kernel spins on this one's progress)
-template <int CELL, int MODE, int N>
+template <int CELL, int MODE, int N, int EG = 1>
 static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUtensorMap& tx, int grid,
                              cudaStream_t s) {
-  using C = TcCfg<MODE, N>;
-  auto k = tc_layer_kernel<CELL, MODE, N>;
+  if constexpr (EG == 1 && MODE != TC_3XTF32) {
+    // bf16 / tf32: the two-epilogue-group variant when the host asks for it
+    // (grid == 0, the preload, loads both)
+    if (grid == 0) {
+      cudaError_t e = launch_tc<CELL, MODE, N, 2>(a, tw, tx, 0, s);
+      if (e != cudaSuccess) return e;
+    } else if (a.egroups == 2) {
+      return launch_tc<CELL, MODE, N, 2>(a, tw, tx, grid, s);
+    }
+  }
+  using C = TcCfg<MODE, N, EG>;
+  auto k = tc_layer_kernel<CELL, MODE, N, EG>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
@@ -322,7 +332,7 @@ static cudaError_t launch_tc(const TcArgs& a, const CUtensorMap& tw, const CUten
   // drains, then wait on griddepcontrol before touching global memory
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kTcThreads);
+  cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attrs[1];

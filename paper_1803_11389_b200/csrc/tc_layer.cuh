@@ -23,9 +23,10 @@
 // are claimed in increasing order and every dependency points to a smaller
 // item, so with all CTAs co-resident the chain cannot deadlock.
 //
-// Roles (192 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer (the converged warp; elect.sync picks the issuing lane), warps 2..5
-// epilogue (TMEM lane quadrant w%4).
+// Roles: warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer (the
+// converged warp; elect.sync picks the issuing lane), then epilogue groups of
+// four warps (TMEM lane quadrant w%4): one group (192 threads) for 3xTF32, two
+// groups taking alternate items (320 threads) for bf16 / tf32.
 #pragma once
 #include <cuda.h>
 
@@ -82,6 +83,7 @@ struct TcArgs {
   int split_start;
   float* fix;
   int* fixflag;
+  int egroups;        // epilogue warp groups in use (1 or 2; <= the kernel's EGROUPS; 0 = all)
   int dbg;            // RNNB_DEBUG bits, timing experiments only (results wrong): 16 no look-back,
                       // 32 no epilogue, 64 no MMAs, 128 no loads, 512 no scan/stores, 1024 no activations
 };
@@ -349,20 +351,20 @@ __device__ __forceinline__ float tc_tanh(float x) {
 __device__ __forceinline__ float tc_sigmoid(float z) { return __fdividef(1.f, 1.f + __expf(-z)); }
 
 // named barrier 2 over the four epilogue warps
-__device__ __forceinline__ void tc_epi_sync() { asm volatile("bar.sync 2, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_epi_sync(int eg = 0) { asm volatile("bar.sync %0, 128;\n" ::"r"(2 + eg) : "memory"); }
 
 // Streaming output: once the 128 epilogue threads stored this item's h rows
 // (ordered by the barrier), one gpu-scope fence and one count per item on
 // the item's output granule; the host's copy-out stream waits until a
 // granule holds nU x (its blocks) counts.
-__device__ __forceinline__ void tc_count_done(const TcArgs& a, int64_t t0, int et) {
+__device__ __forceinline__ void tc_count_done(const TcArgs& a, int64_t t0, int et, int eg = 0) {
   if (a.trace && et == 0) {
     unsigned long long now;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
     atomicMax(&a.trace[1 + a.nB + (int)(t0 / a.T_b)], now);
   }
   if (a.h_done == nullptr) return;
-  tc_epi_sync();
+  tc_epi_sync(eg);
   if (et == 0) {
     __threadfence();
     atomicAdd(&a.h_done[t0 / a.h_gran], 1);
@@ -464,7 +466,7 @@ __host__ __device__ __forceinline__ int x3_chunk_of(int kt) {
   return kt < 2 * RNNB_X3_CK0 ? kt / RNNB_X3_CK0 : 2 + (kt - 2 * RNNB_X3_CK0) / RNNB_X3_CK;
 }
 __host__ __device__ __forceinline__ int x3_nchunks(int nK) { return x3_chunk_of(nK - 1) + 1; }
-template <int MODE, int N>
+template <int MODE, int N, int EG = 1>
 struct TcCfg {
   static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
   static constexpr int A_BYTES = 128 * 128;  // one gate tile: 128 rows x 128 B
@@ -505,6 +507,19 @@ struct TcCfg {
   // a W slot holds one gate's hi + lo tiles (32 KB, freed after that gate's 8
   // MMAs) and the x tiles ([x_hi ; x_lo], shared by the three gates) have
   // their own small ring.
+  // Epilogue warp groups.  The non-chunked modes run TWO groups of four warps
+  // that take alternate items (each on its own TMEM buffers): with short
+  // reductions (cfg3's K = 1024: 5 us of MMAs per item) one group's ~5 us per
+  // item was the bottleneck (cfg3 bf16 T_b = 8 1.41 -> 1.02 ms, tf32 T_b = 32
+  // 0.79 -> 0.57 ms); possible since the look-back needs no barrier across a
+  // group's items any more.  Where the MMA stream bounds an item (cfg2's K =
+  // 2048) the second group gains nothing or costs a few % (tf32 T_b = 64), so
+  // the host picks the one- or the two-group kernel per launch
+  // (TcArgs::egroups; a 320-thread kernel with the second group idle still
+  // cost cfg2 bf16 3 % at T_b = 8-16).  3xTF32 keeps one group (its 254
+  // registers per thread do not fit 320 threads).
+  static constexpr int EGROUPS = CHUNKED ? 1 : EG;  // (EG: template parameter, two kernel variants)
+  static constexpr int THREADS = 64 + 128 * EGROUPS;
   static constexpr bool FINE = CHUNKED;
   static constexpr int W_SLOT = 2 * A_BYTES;
   static constexpr int X_SLOT = SPLIT * B_BYTES;
@@ -545,10 +560,10 @@ __device__ __forceinline__ bool tc_work(const TcArgs& a, int nitems, int k, TcWo
   return false;
 }
 
-template <int CELL, int MODE, int N>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int CELL, int MODE, int N, int EG = 1>
+__global__ void __launch_bounds__((TcCfg<MODE, N, EG>::THREADS), 1)
     tc_layer_kernel(TcArgs a, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX) {
-  using C = TcCfg<MODE, N>;
+  using C = TcCfg<MODE, N, EG>;
   extern __shared__ __align__(1024) unsigned char tsm_raw[];
   unsigned char* tsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(tsm_raw) + 1023) & ~uintptr_t(1023));
   // FINE: full = [W slots | x slots], empty likewise
@@ -777,10 +792,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // c_in (blocked.py:153-162) and the output mix, h stores.
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int row = q * 32 + lane;          // unit within the tile
-    const int et = threadIdx.x - 64;        // 0..127
+    const int eg = (warp - 2) >> 2;         // epilogue group (takes items k = eg mod EGROUPS)
+    const int et = threadIdx.x - 64 - eg * 128;  // 0..127 within the group
+    // groups in use: the second one only pays where the epilogue, not the MMA
+    // stream, bounds an item (short reductions, tiny blocks); the host decides
+    const int neg = (a.egroups >= 1 && a.egroups < C::EGROUPS) ? a.egroups : C::EGROUPS;
     uint32_t acc_it = 0;
     TcWork w;
-    for (int k = 0; tc_work<C::CK>(a, nitems, k, w); ++k) {
+    for (int k = 0; eg < neg && tc_work<C::CK>(a, nitems, k, w); ++k) {
+      if (C::EGROUPS > 1 && (k % neg) != eg) {  // the other group's item (one accumulator buffer each)
+        ++acc_it;
+        continue;
+      }
       const int item = w.item;
       const int b = item / a.nU, u = item - (item / a.nU) * a.nU;
       const int64_t t0 = (int64_t)b * a.T_b;
@@ -1061,7 +1084,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       mbar_arrive(&acc_empty[ab]);
       ++acc_it;
       if (b == a.nB - 1 && a.c_out != nullptr && unit < a.H) a.c_out[unit] = c;  // c_T of the sequence
-      tc_count_done(a, t0, et);
+      tc_count_done(a, t0, et, eg);
     }
   }
   tc_fence_before();
