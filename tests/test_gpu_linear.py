@@ -11,7 +11,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("mode", ["f32", "f64", "bf16", "tf32", "f32x3"])
-@pytest.mark.parametrize("L,d_in,d_out", [(4096, 120, 1024), (300, 1024, 2000), (77, 40, 130), (1, 8, 3)])
+@pytest.mark.parametrize("L,d_in,d_out", [(4096, 120, 1024), (300, 1024, 2000), (77, 40, 130), (1, 8, 3),
+                                         (5003, 200, 777)])
 def test_linear_matches_oracle_gemm(oracle, mode, L, d_in, d_out):
     import torch
     from paper_1803_11389_b200.device import DeviceLinear

@@ -616,6 +616,29 @@ def test_host_streaming_pinned_buffers_zero_copy_output(P, oracle, kind, mode, d
     st.close()
 
 
+@pytest.mark.parametrize("kind,mode,d,L,T", [("qrnn", "bf16", 1024, 3000, 32), ("sru", "tf32", 768, 2500, 8),
+                                             ("sru", "bf16", 512, 4100, 1), ("qrnn", "tf32", 512, 2000, 64)])
+def test_epilogue_groups_are_bitwise_neutral(P, oracle, kind, mode, d, L, T, monkeypatch):
+    """bf16 / tf32: the one- and the two-epilogue-group kernel variants (the
+    second group takes every other item on its own TMEM buffers) compute the
+    same arithmetic in the same order per unit -- bitwise equal outputs and
+    final c, whichever the host would pick."""
+    import torch
+    layers = oracle.generate_layers(kind, d, d, 1, 101, np.float32)
+    X = torch.from_numpy(np.random.default_rng(33).standard_normal((L, d)).astype(np.float32)).cuda()
+    st = P.DeviceStack(kind, layers, mode=mode)
+    outs = []
+    for eg in ("1", "2"):
+        monkeypatch.setenv("RNNB_TC_EGROUPS", eg)
+        c = torch.zeros(d, dtype=torch.float32, device="cuda")
+        H = st.forward(X, T, c_state=c).cpu().numpy()
+        assert st.query(9) == 1
+        outs.append((H, c.cpu().numpy()))
+    assert outs[0][0].tobytes() == outs[1][0].tobytes()
+    assert outs[0][1].tobytes() == outs[1][1].tobytes()
+    st.close()
+
+
 @pytest.mark.timeout(120)
 @pytest.mark.parametrize("mode,T", [("bf16", 16), ("f32", 32), ("tf32", 64)])
 def test_lookback_sentinel_never_collides_with_data(P, oracle, mode, T):
