@@ -278,6 +278,7 @@ rnnb_status linear_forward(rnnb_linear* h, const void* X, int64_t ldx, int64_t L
     a.nU = h->Hpad / 128;
     a.nB = (int)((L + a.T_b - 1) / a.T_b);
     a.egroups = 2;  // dense layers: short K, the store epilogue bounds an item
+    a.ck0 = x3_pick_ck0(a.nK);
     int grid = 0;
     cudaError_t e = tc_layer_run(LINEAR, mode, a, h->Wtc, h->tcKp, h->op, ldop, h->num_sms, s, &grid);
     if (e != cudaSuccess) return fail(RNNB_ECUDA, std::string("tc linear launch: ") + cudaGetErrorString(e));

@@ -434,10 +434,15 @@ rnnb_status tc_layer_launch(rnnb_stack* h, int li, const float* X, int64_t ldx, 
   const int nitems = nU * (int)nB;
   const int G = nitems < h->num_sms - (streaming ? h->stream_free_sms : 0) ? nitems : h->num_sms - (streaming ? h->stream_free_sms : 0);
   a.split_start = nitems;
+  {  // 3xTF32 K-chunk plan (x3_chunk_start): deeper first chunks for short reductions
+    const char* env_ck = getenv("RNNB_X3_CK0");
+    a.ck0 = env_ck ? atoi(env_ck) : x3_pick_ck0(a.nK);
+    if (a.ck0 < 1) a.ck0 = RNNB_X3_CK;
+  }
   const char* env_sp = getenv("RNNB_TC_SPLIT");
   if (mode == TC_3XTF32 && !(env_sp && env_sp[0] == '0')) {
     int W = nitems / G, R = nitems - W * G;
-    const int nch = x3_nchunks(a.nK);
+    const int nch = x3_nchunks(a.nK, a.ck0);
     if (streaming && nitems > G) {
       // input-bound launch (rows arrive slower than the kernel consumes them):
       // what counts is how soon the LAST blocks finish after their rows land,

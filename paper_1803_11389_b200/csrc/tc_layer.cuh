@@ -83,6 +83,7 @@ struct TcArgs {
   int split_start;
   float* fix;
   int* fixflag;
+  int ck0;            // 3xTF32: k-tiles in each of an item's first two K chunks (x3_chunk_start)
   int egroups;        // epilogue warp groups in use (1 or 2; <= the kernel's EGROUPS; 0 = all)
   int dbg;            // RNNB_DEBUG bits, timing experiments only (results wrong): 16 no look-back,
                       // 32 no epilogue, 64 no MMAs, 128 no loads, 512 no scan/stores, 1024 no activations
@@ -448,24 +449,27 @@ __device__ __forceinline__ float tc_lookback(const TcArgs& a, int b, int u, int 
 #ifndef RNNB_X3_CK
 #define RNNB_X3_CK 8  // 3xTF32 K chunk in k-tiles (8 x 32 = 256-deep; 128-deep: 8 % slower, half the error)
 #endif
-#ifndef RNNB_X3_CK0
-#define RNNB_X3_CK0 RNNB_X3_CK  // the FIRST TWO chunks of an item may be longer (experiment, see below)
-#endif
-// 3xTF32 chunk plan of an item's nK k-tiles: two chunks of CK0 k-tiles, then
-// chunks of CK.  While the epilogue warps finish an item (activations,
-// look-back, scan, stores) the MMA warp can run only two chunks of the next
-// item ahead (two TMEM buffers; TMEM is full).  Longer first chunks (CK0 = 12)
-// were tried to buy slack there: cfg2 T_b=32 209.2 -> 205.8 us, but 25 % more
-// accumulation error (cfg2 9.8e-7 -> 1.2e-6, cfg4 4.2e-6 -> 4.6e-6) -- not
-// worth it, so CK0 = CK; the look-back's cost (~10 us per launch) is the tail
-// after the last wave, not a per-item stall.
-__host__ __device__ __forceinline__ int x3_chunk_start(int c) {
-  return c <= 2 ? c * RNNB_X3_CK0 : 2 * RNNB_X3_CK0 + (c - 2) * RNNB_X3_CK;
+// 3xTF32 chunk plan of an item's nK k-tiles: two chunks of ck0 k-tiles, then
+// chunks of CK (ck0 = TcArgs::ck0, chosen by the host).  While the epilogue
+// warps finish an item (activations, look-back, scan, stores) the MMA warp
+// can run only two chunks of the next item ahead (two TMEM buffers; TMEM is
+// full), and every chunk costs the epilogue a TMEM read + add pass.
+//  * Short reductions (nK <= 32, i.e. K <= 1024: cfg3): ck0 = 16 -- an item is
+//    two 512-deep chunks instead of four 256-deep ones: cfg3 f32 T_b = 32
+//    1.81 -> 1.30 ms, T_b = 8 4.44 -> 3.97 ms; the total depth is small, so
+//    the accumulation error stays low (cfg3 logits within the fp32 bound).
+//  * Long reductions (cfg2, cfg4): ck0 = CK = 8.  Longer first chunks there
+//    were measured: 12: 1.6 % faster, 25 % more error; 16: slower (207 vs
+//    198 us) and cfg4's 8-layer error 4.2e-6 -> 5.4e-6 -- not adopted.
+__host__ __device__ __forceinline__ int x3_chunk_start(int c, int ck0) {
+  return c <= 2 ? c * ck0 : 2 * ck0 + (c - 2) * RNNB_X3_CK;
 }
-__host__ __device__ __forceinline__ int x3_chunk_of(int kt) {
-  return kt < 2 * RNNB_X3_CK0 ? kt / RNNB_X3_CK0 : 2 + (kt - 2 * RNNB_X3_CK0) / RNNB_X3_CK;
+__host__ __device__ __forceinline__ int x3_chunk_of(int kt, int ck0) {
+  return kt < 2 * ck0 ? kt / ck0 : 2 + (kt - 2 * ck0) / RNNB_X3_CK;
 }
-__host__ __device__ __forceinline__ int x3_nchunks(int nK) { return x3_chunk_of(nK - 1) + 1; }
+__host__ __device__ __forceinline__ int x3_nchunks(int nK, int ck0) { return x3_chunk_of(nK - 1, ck0) + 1; }
+__host__ __device__ __forceinline__ int x3_pick_ck0(int nK) { return nK <= 32 ? 16 : RNNB_X3_CK; }
+
 template <int MODE, int N, int EG = 1>
 struct TcCfg {
   static constexpr int ES = TcT<MODE>::ES, KT = TcT<MODE>::KT, UK = TcT<MODE>::UK;
@@ -552,7 +556,7 @@ __device__ __forceinline__ bool tc_work(const TcArgs& a, int nitems, int k, TcWo
     return true;
   }
   if (k == nwhole && a.split_start < nitems && bx < 2 * (nitems - a.split_start)) {
-    const int kmid = x3_chunk_start(x3_nchunks(a.nK) / 2);
+    const int kmid = x3_chunk_start(x3_nchunks(a.nK, a.ck0) / 2, a.ck0);
     const int part = bx & 1;
     w = TcWork{a.split_start + bx / 2, part ? kmid : 0, part ? a.nK : kmid, part};
     return true;
@@ -718,9 +722,9 @@ __global__ void __launch_bounds__((TcCfg<MODE, N, EG>::THREADS), 1)
           tc_fence_after();
         }
         for (int kt = w.kt0; kt < w.kt1; ++kt, ++it) {
-          const int kch = C::CHUNKED ? x3_chunk_of(kt) : 0;
-          const int kc = C::CHUNKED ? kt - x3_chunk_start(kch) : kt;  // k-tile index inside the accumulation
-          const bool kc_last = C::CHUNKED && (kt + 1 == x3_chunk_start(kch + 1) || kt == w.kt1 - 1);
+          const int kch = C::CHUNKED ? x3_chunk_of(kt, a.ck0) : 0;
+          const int kc = C::CHUNKED ? kt - x3_chunk_start(kch, a.ck0) : kt;  // k-tile index inside the accumulation
+          const bool kc_last = C::CHUNKED && (kt + 1 == x3_chunk_start(kch + 1, a.ck0) || kt == w.kt1 - 1);
           if (C::CHUNKED && kc == 0) {  // a new K-chunk accumulates into a fresh buffer
             ab = acc_it % C::NACC;
             dbase = tmem + ab * C::ACC_COLS;
@@ -810,7 +814,7 @@ __global__ void __launch_bounds__((TcCfg<MODE, N, EG>::THREADS), 1)
       const int l = (int)((a.L - t0) < a.T_b ? (a.L - t0) : a.T_b);
       const int unit = u * 128 + row;
       if (a.dbg & 32) {  // timing experiment: epilogue only hands the accumulators back
-        const int nacc = C::CHUNKED ? x3_chunk_of(w.kt1 - 1) - x3_chunk_of(w.kt0) + 1 : 1;
+        const int nacc = C::CHUNKED ? x3_chunk_of(w.kt1 - 1, a.ck0) - x3_chunk_of(w.kt0, a.ck0) + 1 : 1;
         for (int ch = 0; ch < nacc; ++ch, ++acc_it) {
           const int ab = acc_it % C::NACC;
           mbar_wait(&acc_full[ab], (acc_it / C::NACC) & 1);
@@ -857,7 +861,7 @@ __global__ void __launch_bounds__((TcCfg<MODE, N, EG>::THREADS), 1)
         float rz[N], rf[N], ro[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) rz[j] = rf[j] = ro[j] = 0.f;
-        const int nch = x3_nchunks(a.nK);
+        const int nch = x3_nchunks(a.nK, a.ck0);
         const int hch = nch / 2;  // first chunk of the second half (see tc_work)
         const int c_lo = w.part == 1 ? hch : 0, c_hi = w.part == 0 ? hch : nch;
         // the first half's sum waits in TMEM columns past the accumulators
