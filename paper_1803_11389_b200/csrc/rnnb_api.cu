@@ -1034,8 +1034,14 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       tev.push_back(e);
       tname.push_back(name);
     };
+    const bool trace_host = trace && atoi(getenv("RNNB_STREAM_TRACE")) >= 3;  // 3: host-side time stamps only
+    std::vector<std::pair<const char*, double>> hts;
+    auto hmark = [&](const char* name) {
+      if (trace_host) hts.emplace_back(name, std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_call).count());
+    };
+    hmark("entry + setup");
     mark(s, "start");
-    if (trace) {
+    if (trace && !trace_host) {
       if (h->stream_trace) cudaFree(h->stream_trace);
       CUDA_TRY(cudaMalloc(&h->stream_trace, (1 + 2 * nBt) * sizeof(unsigned long long)));
       CUDA_TRY(cudaMemset(h->stream_trace, 0, (1 + 2 * nBt) * sizeof(unsigned long long)));
@@ -1135,12 +1141,14 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       if ((st = copy_in(i)) != RNNB_OK) return st;
       if (i == 0 && conv_first && (st = launch_conv()) != RNNB_OK) return st;
     }
+    hmark("copies enqueued (pre)");
     h->stream_ready = h->stream_ctr;
     h->stream_done = dHz ? nullptr : h->stream_ctr + 2;
     h->stream_chunk = (int)g;
     mark(s, "before layer kernel");
     st = rnnb_forward(h, dX, din, L, block_size, dHz ? dHz : dH, dh, dC, dXC, stream);
     mark(s, "layer kernel done");
+    hmark("layer kernel launched");
     if (st == RNNB_OK && !conv_first && (st = launch_conv()) != RNNB_OK) return st;
     h->stream_ready = nullptr;
     h->stream_done = nullptr;
@@ -1174,7 +1182,10 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     CUDA_TRY(cudaEventRecord(ev_done, h->s_in2));
     CUDA_TRY(cudaStreamWaitEvent(s, ev_done, 0));
     mark(s, "all done");
+    hmark("everything enqueued");
     CUDA_TRY(cudaStreamSynchronize(s));
+    hmark("synchronised");
+    for (auto& t : hts) fprintf(stderr, "[rnnb stream trace] host %8.1f us  %s\n", t.second, t.first);
     // The time-out flag is set only by a kernel thread that waited
     // kStreamTimeoutNs (2 s) for rows: a call that returned sooner cannot have
     // failed, and skips the flag's copy-out (a copy-engine round trip behind
@@ -1184,7 +1195,7 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       CUDA_TRY(cudaMemcpyAsync(h->stream_flag_host, h->stream_ctr + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
       CUDA_TRY(cudaStreamSynchronize(s));
     }
-    if (trace) {
+    if (trace && !trace_host) {
       for (size_t i = 1; trace_ev && i < tev.size(); ++i) {
         float ms = 0.f;
         cudaEventElapsedTime(&ms, tev[0], tev[i]);
