@@ -45,6 +45,9 @@ max(shared-memory weight stream, FMA pipe) for the FFMA kernels.
   reference-signature drop-in `run_blocked` (weights re-uploaded and repacked
   on the GPU per call): {d['dropin']['ms_per_call']:.1f} ms per call = {d['dropin']['value'] / 1e3:.0f} k steps/s (83 ms before
   the GPU repack).
+* Box to box (same final binary, five bench runs this round): device 9.47-9.66 M
+  steps/s, e2e 5.2-5.5 M on four boxes and 2.5-3.8 M on the slow-host box of
+  §4.5.
 * ncu launch list of the bench command (`profiles/ncu_launches_r2.csv`,
   summary beside it): the 3xTF32 `tc_layer_kernel` 88 % of GPU time (219 µs
   per cold launch), the L2 flush fill 6 %, the one-time weight repack 4 %,
