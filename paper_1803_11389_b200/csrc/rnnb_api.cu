@@ -931,7 +931,15 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
   char* hH = static_cast<char*>(H);
   char* dH = static_cast<char*>(h->hostH);
   const int64_t T = block_size < 1 ? 1 : block_size;
-  if (!c_state && !x_carry) {
+  // no state in or out and the tensor-core streaming path: the layer launch
+  // takes null state pointers (zero c_0 / x_{-1}, no c_T copy) -- two host
+  // calls less before the launch
+  const bool want_state = c_state != nullptr || x_carry != nullptr;
+  const bool tc_stream_candidate = !h->stream_disabled.load() && h->n_layers == 1 &&
+                                   use_tc_layer(h, h->layers[0], L, block_size < 1 ? 1 : block_size) && h->num_sms > 8 &&
+                                   !(getenv("RNNB_HOST_STREAM") && getenv("RNNB_HOST_STREAM")[0] == '0');
+  if (!want_state && tc_stream_candidate) {
+  } else if (!c_state && !x_carry) {
     CUDA_TRY(cudaMemsetAsync(dC, 0, (csz + xsz) * es, s));  // dC, dXC are adjacent: one call
   } else {
     if (c_state) CUDA_TRY(cudaMemcpyAsync(dC, c_state, csz * es, cudaMemcpyHostToDevice, s));
@@ -999,7 +1007,6 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev_start, 0));
     CUDA_TRY(cudaStreamWaitEvent(h->s_in2, ev_start, 0));
     CUDA_TRY(cudaStreamWaitEvent(h->s_cv, ev_start, 0));
-    CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
     const float* fX = reinterpret_cast<const float*>(dX);
     const float* fXC = reinterpret_cast<const float*>(dXC);
     // Output straight into the caller's buffer when it is pinned (mapped)
@@ -1020,6 +1027,7 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       else
         (void)cudaGetLastError();
     }
+    if (!dHz) CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev_start, 0));
     // RNNB_STREAM_TRACE=1: timing events after every copy / conversion and
     // around the layer kernel, printed relative to the call's start (tuning only)
     const bool trace = getenv("RNNB_STREAM_TRACE") != nullptr;
@@ -1079,6 +1087,8 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     }
     ++h->stream_epoch;
     const bool conv_stream = tc_to_operand_stream_ok(fX, din, h->kind == RNNB_QRNN ? fXC : nullptr, h->op, ldop, (int)din);
+    // (without the persistent conversion the per-segment fallback reads the carry buffer: keep it defined)
+    if (!conv_stream && !want_state) CUDA_TRY(cudaMemsetAsync(dC, 0, (csz + xsz) * es, s));
     auto copy_in = [&](int64_t i) -> rnnb_status {
       const int64_t t0 = seg[i], n = seg[i + 1] - seg[i];
       // segments alternate between two copy streams: a stream's write-value
@@ -1118,8 +1128,8 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
       const char* env_n = getenv("RNNB_STREAM_CTAS");
       int workers = env_n ? atoi(env_n) : 12;
       if (workers < 1) workers = 1;
-      CUDA_TRY(tc_to_operand_stream(mode, fX, din, h->kind == RNNB_QRNN ? fXC : nullptr, h->op, ldop, L, (int)din,
-                                    segtab, seg_flag, h->stream_ctr, h->stream_ctr + 1, h->stream_flags, copied_ctr + 1,
+      CUDA_TRY(tc_to_operand_stream(mode, fX, din, h->kind == RNNB_QRNN && want_state ? fXC : nullptr, h->op, ldop, L,
+                                    (int)din, segtab, seg_flag, h->stream_ctr, h->stream_ctr + 1, h->stream_flags, copied_ctr + 1,
                                     h->stream_epoch, group, workers, h->s_cv));
       mark(h->s_cv, "conversion kernel done");
       return RNNB_OK;
@@ -1146,7 +1156,8 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     h->stream_done = dHz ? nullptr : h->stream_ctr + 2;
     h->stream_chunk = (int)g;
     mark(s, "before layer kernel");
-    st = rnnb_forward(h, dX, din, L, block_size, dHz ? dHz : dH, dh, dC, dXC, stream);
+    st = rnnb_forward(h, dX, din, L, block_size, dHz ? dHz : dH, dh, want_state ? dC : nullptr,
+                      want_state ? dXC : nullptr, stream);
     mark(s, "layer kernel done");
     hmark("layer kernel launched");
     if (st == RNNB_OK && !conv_first && (st = launch_conv()) != RNNB_OK) return st;
@@ -1226,6 +1237,9 @@ static rnnb_status rnnb_forward_host_impl(rnnb_stack_t h, const void* X, int64_t
     h->stream_disabled.store(true);  // rows arrived too late (serialising profiler): redo without streaming
     return rnnb_forward_host_impl(h, X, L, block_size, H, c_state, x_carry, stream);
   }
+
+  // (the tensor-core streaming path was not taken after all: the other paths read the state buffers)
+  if (!want_state && tc_stream_candidate) CUDA_TRY(cudaMemsetAsync(dC, 0, (csz + xsz) * es, s));
 
   // Streaming (single-layer fp32 stacks, warp-specialised kernel): ONE layer
   // launch consumes X while it is still being copied in -- its TMA producer
